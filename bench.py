@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the GTC hot path: encode -> exchange -> decode_apply.
+
+One "step" = one pass of the whole hot path over one synthetic gradient per
+rank: residual accumulate + threshold + quantize + pack + compact (encode), the
+NCCL all-gather of the messages (exchange, world > 1), integer aggregation +
+sparse apply to the replicated weights (decode_apply).
+
+Metric (BASELINE.json): params/sec of encode+exchange+apply per step, whole job
+(= world * n_params / step time, weak scaling: every rank owns a full gradient).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gtc|reference]
+                    [--workload lstm_am|lstm_am_30m|1e9] [--rho 0.01] [--cmp gt|ge]
+
+N > 1 is launched by torchrun (RANK/LOCAL_RANK/WORLD_SIZE from the env).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "params/sec encode+exchange+apply per step"
+UNIT = "params/s"
+N_GRAD_BUFFERS = 3  # gradients rotate so each step reads a fresh 4n bytes
+
+WORKLOADS = {
+    # C2 (BASELINE configs[1]): the paper-shaped LSTM AM
+    "lstm_am": dict(n=synth.LSTM_AM_PARAMS, desc="LSTM-AM gradient, 5x768 LSTM + 3183 senones (24,286,575 params)"),
+    # north_star's "~30M params" variant
+    "lstm_am_30m": dict(n=30_000_000, desc="LSTM-AM-shaped gradient padded to 30,000,000 params"),
+    # C5: 1B params per rank
+    "1e9": dict(n=1_000_000_000, desc="1e9-param synthetic gradient (HBM-bound regime)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["gtc", "reference"], default="gtc")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="lstm_am")
+    ap.add_argument("--rho", type=float, default=0.01, help="target per-rank update density")
+    ap.add_argument("--tau", type=float, default=8.0, help="gradient threshold (PAPER.md:249 uses 8)")
+    ap.add_argument("--cmp", choices=["gt", "ge"], default="gt")
+    ap.add_argument("--alpha", type=float, default=-1e-3, help="apply scale (e.g. -lr)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms in the background."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self):
+        self.marks.append(time.time())
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        t0, t1 = (self.marks + [0, 0])[:2] if len(self.marks) >= 2 else (0, 1e30)
+        inside = [r for t, r in self.rows if t0 <= t <= t1 + 0.2] or [r for _, r in self.rows]
+        sm = [float(r[1]) for r in inside if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in inside if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in inside for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(inside)}
+
+
+def make_inputs(n, tau, rho, rank, world):
+    """Per-rank synthetic inputs (host): 3 LSTM-shaped gradients, r0 ~ U(-tau, tau), w0."""
+    sigma = synth.sigma_for_density(rho, tau, synth.mean_abs_scale(n))
+    corr = 0.5 if world > 1 else 0.0
+    grads = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, rank, corr) for t in range(N_GRAD_BUFFERS)]
+    r0 = synth.uniform(n, -tau, tau, synth.rank_seed(rank))
+    w0 = synth.normal(n, synth.BASE_SEED, 0, 11) * np.float32(0.05)  # replicated weights
+    return grads, r0, w0
+
+
+# ------------------------------------------------------------------ oracle legs
+def cpu_oracle_run(n_full, tau, rho, cmp, alpha, budget_s, world=1):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
+    import oracle
+
+    cores = 1  # oracle.step is single-threaded
+    n = n_full
+    grads, r0, w0 = make_inputs(n, tau, rho, 0, 1)
+    gs = [grads[t % N_GRAD_BUFFERS] for t in range(N_GRAD_BUFFERS)]
+    rs = [r0.copy() for _ in range(world)]
+    w = w0.copy()
+    mode = oracle.CMP_GT if cmp == "gt" else oracle.CMP_GE
+    steps, t_used = 0, 0.0
+    while t_used < budget_s or steps < 1:
+        g = [gs[steps % N_GRAD_BUFFERS]] * world
+        t0 = time.perf_counter()
+        oracle.step(g, rs, w, tau, mode, alpha, oracle.ACCUM_WEIGHTS)
+        t_used += time.perf_counter() - t0
+        steps += 1
+        if steps >= 200:
+            break
+    value = world * n * steps / t_used
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{steps} full steps of the {n}-param workload x {world} simulated worker(s) "
+                      f"(oracle.step: encode+aggregate+apply, single thread), {t_used:.1f} s"}
+
+
+def run_reference(args):
+    rank, local_rank, world = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+
+    wl = WORKLOADS[args.workload]
+    n_full = wl["n"]
+    # per-step sample sized so warmup+steps finish in about a minute
+    per_param = 8e-9
+    budget = 60.0
+    n = int(min(n_full, max(65_536, budget / max(1, args.steps + args.warmup) / per_param)))
+    grads, r0, w0 = make_inputs(n, args.tau, args.rho, 0, 1)
+    mode = oracle.CMP_GT if args.cmp == "gt" else oracle.CMP_GE
+    rs = [r0.copy() for _ in range(world)]
+    w = w0.copy()
+    for t in range(args.warmup):
+        oracle.step([grads[t % N_GRAD_BUFFERS]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
+    t0 = time.perf_counter()
+    for t in range(args.steps):
+        oracle.step([grads[t % N_GRAD_BUFFERS]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
+    dt = time.perf_counter() - t0
+    value = world * n * args.steps / dt
+    sample = f"each step: {n} of {n_full} params x {world} simulated worker(s), oracle.step single thread"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": args.workload, "n_params": n_full, "sample_params": n,
+                                        "tau": args.tau, "rho_target": args.rho, "cmp": args.cmp},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_gtc(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1904_10584_b200 as gtc
+
+    rank, local_rank, world = dist_env()
+    if world != args.gpus and not (world == 1 and args.gpus == 1):
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    wl = WORKLOADS[args.workload]
+    n, tau = wl["n"], args.tau
+    grads_h, r0_h, w0_h = make_inputs(n, tau, args.rho, rank, world)
+    grads = [torch.from_numpy(g).to(dev) for g in grads_h]
+    r = torch.from_numpy(r0_h).to(dev)
+    w = torch.from_numpy(w0_h).to(dev)
+    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(t):
+        ctx.encode(grads[t % N_GRAD_BUFFERS], r)
+        ctx.exchange()
+        ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
+
+    for t in range(max(3, args.warmup)):
+        step(t)
+    torch.cuda.synchronize()
+
+    # per-kernel events inside the timed region (on the stream the kernels run on)
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kptr = ctx.local_count_tensor()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.6)
+    launches0 = ctx.kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark()
+    e_start.record(stream)
+    for t in range(K):
+        ev[t][0].record(stream)
+        ctx.encode(grads[t % N_GRAD_BUFFERS], r)
+        ev[t][1].record(stream)
+        ctx.exchange()
+        ev[t][2].record(stream)
+        ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
+        ev[t][3].record(stream)
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.mark()
+    launches = ctx.kernel_launches() - launches0
+    time.sleep(0.3)
+    clocks.stop()
+
+    ms_local = e_start.elapsed_time(e_end)
+    enc_ms = sum(ev[t][0].elapsed_time(ev[t][1]) for t in range(K)) / K
+    exch_ms = sum(ev[t][1].elapsed_time(ev[t][2]) for t in range(K)) / K
+    dec_ms = sum(ev[t][2].elapsed_time(ev[t][3]) for t in range(K)) / K
+    ks_local = ctx.last_counts()
+    k_rank = ks_local[rank] if world > 1 else ks_local[0]
+
+    # density of the touched set (for the decode's algorithmic bytes), untimed
+    cnt = torch.empty(n, dtype=torch.int8, device=dev)
+    ctx.encode(grads[K % N_GRAD_BUFFERS], r)
+    ctx.exchange()
+    ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS, cnt)
+    nnz_c = int(torch.count_nonzero(cnt).item())
+    k_all = ctx.last_counts()
+    del cnt
+
+    stats = torch.tensor([ms_local, enc_ms, exch_ms, dec_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    ms, enc_ms_max, exch_ms_max, dec_ms_max = stats.tolist()
+    ms_per_step = ms / K
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(g).pin_memory() for g in grads_h]
+        k_host = torch.zeros(1, dtype=torch.int64).pin_memory()
+        gdev = torch.empty(n, dtype=torch.float32, device=dev)
+        E = args.e2e_steps
+        for t in range(2):
+            gdev.copy_(pinned[t % N_GRAD_BUFFERS], non_blocking=True)
+            ctx.step(gdev, r, w, args.alpha)
+            k_host.copy_(kptr, non_blocking=True)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for t in range(E):
+            gdev.copy_(pinned[t % N_GRAD_BUFFERS], non_blocking=True)
+            ctx.step(gdev, r, w, args.alpha)
+            k_host.copy_(kptr, non_blocking=True)
+            stream.synchronize()
+            _ = int(k_host[0])
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([s0.elapsed_time(s1) / E], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n / (e2e_ms.item() * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,
+               "ms_per_step": e2e_ms.item(),
+               "note": "pinned host gradient -> device copy + encode/exchange/decode_apply + k read back, per step"}
+        del gdev
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        ctx.close()
+        return 0
+
+    # ---- roofline of the dominant kernel (encode) and the decode
+    peak, peak_src = measured_peaks()
+    ntiles = math.ceil(n / gtc.GTC_TILE)
+    enc_bytes = 12 * n + 4 * k_rank + 4 * (ntiles + 1)
+    enc_gbs = enc_bytes / (enc_ms * 1e-3) / 1e9
+    sum_k = sum(k_all)
+    dec_bytes = 4 * sum_k + 4 * world * (ntiles + 1) + 8 * nnz_c
+    dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9 if dec_ms > 0 else None
+    step_bytes = enc_bytes + dec_bytes + (4 * (world - 1) * max(k_all) if world > 1 else 0)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "encode_dram_bytes.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            if tj.get("workload") == args.workload and tj.get("n") == n:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_oracle_run(n, tau, args.rho, args.cmp, args.alpha, args.cpu_seconds)
+
+    value = world * n / (ms_per_step * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, args.warmup),
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": wl["desc"], "n_params": n, "tau": tau,
+                   "rho_target": args.rho, "rho_measured": k_rank / n, "cmp": args.cmp,
+                   "parallelism": f"dp{world}", "apply": "ACCUM_WEIGHTS",
+                   "l2": f"inputs larger than L2: g rotates over {N_GRAD_BUFFERS} buffers, "
+                         f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},
+        "roofline": {"bound": "hbm", "kernel": "gtc_encode_kernel", "achieved": enc_gbs, "peak": peak,
+                     "unit": "GB/s", "frac": enc_gbs / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": enc_bytes, "ms_per_launch": enc_ms,
+                     "peak_source": peak_src,
+                     "share_of_step": enc_ms / ms_per_step},
+        "kernels": {"encode_ms": enc_ms, "exchange_ms": exch_ms, "decode_apply_ms": dec_ms,
+                    "decode_apply_GBs": dec_gbs, "decode_alg_bytes": dec_bytes, "nnz_counts": nnz_c,
+                    "k_per_rank": k_all,
+                    "step_alg_bytes": step_bytes,
+                    "step_hbm_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gtc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,189 @@
+/*
+ * gtc.h -- C ABI of libgtc.so: the B200 hot path of Gradient Threshold
+ * Compression (GTC), PAPER.md:221-222 (Sec. VI-A "Gradient Threshold
+ * Compression", arXiv 1904.10584).
+ *
+ * One synchronous data-parallel step on every rank ("we select the
+ * synchronous variant"):
+ *
+ *   gtc_encode        residual += grad; every element with |residual| > tau
+ *                     (or >= tau, GTC_CMP_GE) sends ONE quantum +-tau and keeps
+ *                     the rest; the survivors are packed into 32-bit words
+ *                     (index << 1 | negative) in ascending index order.
+ *                     P:222 "only gradient elements whose absolute magnitude is
+ *                     greater than a constant ... (tau) are sent", "The residual
+ *                     gradients which are not sent ... are aggregated locally",
+ *                     "1-bit quantization ... deltas of +-tau", "packing quantized
+ *                     gradient and integer index into single 32-bit integer field".
+ *   gtc_exchange      all-gather of every rank's message over NCCL/NVLink.
+ *                     P:222 "Each worker communicates the sparse update to all
+ *                     other workers and conversely receives all sparse updates".
+ *   gtc_decode_apply  signed integer count c[i] in [-N, N] of the quanta every
+ *                     rank sent for element i, then target[i] is updated by
+ *                     c[i]*tau.  P:222 "The received sparse gradient updates are
+ *                     aggregated and weights are updated based on the aggregate".
+ *
+ * Readings the paper leaves open (R1..R10): strict vs. non-strict
+ * threshold (flag), word layout, one quantum per element per step, integer
+ * counts as the aggregate, the apply arithmetic
+ *     u = fl((float)c * tau);   WEIGHTS: t = fmaf(alpha, u, t);   UPDATE: t = fl(t + u)
+ * applied only where c != 0, IEEE fp32 RNE with denormals kept.
+ *
+ * Conventions
+ *  - Memory: every device pointer is CUDA device memory OWNED BY THE CALLER.
+ *    libgtc never calls cudaMalloc/cudaFree.  Its scratch ("workspace") is one
+ *    caller allocation whose size gtc_workspace_size() reports and which
+ *    gtc_bind_workspace() hands over for the life of the context.  The context
+ *    owns its NCCL communicator and one small pinned host buffer.
+ *  - Streams: every call that takes a stream enqueues device work on it and
+ *    returns without waiting, EXCEPT gtc_exchange with world > 1 (one host wait
+ *    for the per-rank word counts), gtc_decode_apply_msgs (validates the
+ *    messages, waits) and gtc_check (waits).  Consecutive calls on one context
+ *    must be ordered (same stream, or caller-ordered streams).
+ *  - Order: gtc_init -> gtc_workspace_size -> gtc_bind_workspace ->
+ *    (gtc_encode -> gtc_exchange -> gtc_decode_apply)*.  Out-of-order calls
+ *    return GTC_ESTATE.  gtc_decode_apply_msgs may be called any time after bind.
+ *  - Alignment: grad/residual/target must be 16-byte aligned (GTC_EALIGN);
+ *    n need not be a multiple of 4.
+ *  - Errors: no exception or abort crosses the ABI.  Device-side conditions
+ *    (non-finite residual seen, message overflowing the capacity, corrupt
+ *    message) set sticky flags, reported by gtc_exchange (world > 1) or
+ *    gtc_check (any world), and cleared once reported.
+ */
+#ifndef GTC_H
+#define GTC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gtc_ctx gtc_ctx; /* opaque; one per rank */
+
+typedef enum {
+    GTC_OK = 0,
+    GTC_EINVAL = 1,      /* bad argument (tau <= 0 or non-finite, bad mode, NULL) */
+    GTC_EDIM = 2,        /* n_params < 0 or >= 2^31 (31-bit index field)         */
+    GTC_EALIGN = 3,      /* a pointer is not 16-byte aligned                      */
+    GTC_ECUDA = 4,       /* a CUDA runtime call failed (see gtc_last_error_detail) */
+    GTC_ENCCL = 5,       /* an NCCL call failed                                   */
+    GTC_ENONFINITE = 6,  /* a NaN/Inf residual was seen (step still completed:
+                            NaN is never sent, +-Inf is sent every step)          */
+    GTC_ECORRUPT = 7,    /* a message word is out of range or not ascending      */
+    GTC_ESTATE = 8,      /* call out of order / workspace not bound              */
+    GTC_ECAPACITY = 9,   /* a message exceeded max_words_per_rank                 */
+    GTC_EUNSUPPORTED = 10 /* e.g. world > GTC_MAX_MSGS                           */
+} gtc_status;
+
+/* Threshold comparison (R1). */
+enum { GTC_CMP_GT = 0, /* paper, "greater than": |v| > tau (default) */
+       GTC_CMP_GE = 1  /* BASELINE.json north_star: |v| >= tau             */ };
+
+/* What decode_apply updates (R8). */
+enum { GTC_ACCUM_WEIGHTS = 0, /* target[i] = fmaf(alpha, fl(c[i]*tau), target[i]) */
+       GTC_ACCUM_UPDATE = 1   /* target[i] = fl(target[i] + fl(c[i]*tau))        */ };
+
+/* Most messages one decode_apply can aggregate (ranks or simulated workers). */
+#define GTC_MAX_MSGS 64
+/* Parameters per tile of the encode/decode kernels; tile offsets are per tile. */
+#define GTC_TILE 4096
+
+/* Fill 128 bytes with a fresh NCCL unique id (rank 0 calls it and broadcasts
+ * the bytes to the other ranks, e.g. over a torch.distributed group). */
+gtc_status gtc_get_unique_id(void* out_128_bytes);
+
+/* Create a context for one rank.
+ *  n_params   : length of the flat parameter vector ("for each trainable
+ *               weight" -- one global index space, R7), 0 <= n < 2^31.
+ *  tau        : the gradient threshold (P:249 uses 8), finite, > 0.
+ *  rank/world : this process's rank, number of data-parallel workers.
+ *  nccl_unique_id : 128 bytes from gtc_get_unique_id on rank 0; NULL iff world == 1.
+ *  cuda_device: device ordinal this rank runs on (made current for the call).
+ *  flags      : GTC_CMP_GT or GTC_CMP_GE.
+ * On success *out is a new context (free with gtc_destroy). Blocks on NCCL
+ * communicator creation when world > 1. */
+gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int world,
+                    const void* nccl_unique_id, int cuda_device, uint32_t flags);
+
+/* Bytes of device workspace needed for messages of at most max_words_per_rank
+ * words (<= 0 means n_params, which can never overflow) and for
+ * gtc_decode_apply_msgs calls of up to max_sim_msgs messages (0 allowed). */
+gtc_status gtc_workspace_size(const gtc_ctx* ctx, int64_t max_words_per_rank,
+                              int max_sim_msgs, size_t* bytes);
+
+/* Hand the workspace to the context (256-byte aligned, >= the size above for
+ * the SAME max_words_per_rank / max_sim_msgs).  Initialises it with a
+ * synchronous cudaMemset.  The caller keeps ownership and must keep it alive
+ * until gtc_destroy. */
+gtc_status gtc_bind_workspace(gtc_ctx* ctx, void* dev_ptr, size_t bytes,
+                              int64_t max_words_per_rank, int max_sim_msgs);
+
+/* Steps 1-4 of P:222 for this rank, one fused kernel on `stream`.
+ *  grad     : float[n] device, read only; NULL means residual already holds
+ *             residual + grad (the caller accumulated into it).
+ *  residual : float[n] device, in/out; the caller zeroes it once at the start
+ *             of training (R5) and checkpoints it with the weights.
+ * The message (uint32 words, ascending index), its length k and per-tile
+ * offsets stay in the workspace (see gtc_message / gtc_local_count). */
+gtc_status gtc_encode(gtc_ctx* ctx, const float* grad, float* residual, cudaStream_t stream);
+
+/* All-gather of every rank's message (world > 1): ncclAllGather of (k, flags),
+ * ONE host wait for the counts, then ncclAllGather of the words padded to the
+ * largest k and of the per-tile offsets.  world == 1: no device work.
+ * Returns GTC_ENONFINITE if any rank flagged a non-finite residual (the
+ * exchange still completed; decode_apply may proceed), GTC_ECAPACITY if any
+ * rank's k exceeded the capacity (nothing exchanged). */
+gtc_status gtc_exchange(gtc_ctx* ctx, cudaStream_t stream);
+
+/* Steps 5-6 of P:222 on `stream`: signed integer counts of all ranks' quanta
+ * (deterministic, atomic-free, rank order irrelevant) and the apply of
+ * count * tau to target (float[n] device, in/out) for every element with a
+ * non-zero count (mode GTC_ACCUM_WEIGHTS with alpha, or GTC_ACCUM_UPDATE).
+ * counts_out: int8[n] device or NULL; if given receives every count (debug /
+ * parity; costs n extra bytes written). */
+gtc_status gtc_decode_apply(gtc_ctx* ctx, float* target, float alpha, int mode,
+                            int8_t* counts_out, cudaStream_t stream);
+
+/* Same aggregate+apply over caller-supplied messages, no NCCL: used for
+ * simulated workers on one GPU and for tests.
+ *  msgs   : host array of nmsg DEVICE pointers to uint32 words (ascending)
+ *  counts : host array of nmsg word counts
+ * Validates every message (GTC_ECORRUPT on a word with index >= n or a
+ * non-increasing index; nothing is applied then) and waits for the stream. */
+gtc_status gtc_decode_apply_msgs(gtc_ctx* ctx, const uint32_t* const* msgs,
+                                 const int64_t* counts, int nmsg, float* target,
+                                 float alpha, int mode, int8_t* counts_out,
+                                 cudaStream_t stream);
+
+/* Per-rank word counts of the last gtc_exchange (world entries; for world == 1
+ * this reads the local count back and waits on the last encode's stream). */
+gtc_status gtc_last_counts(gtc_ctx* ctx, int64_t* k_per_rank);
+
+/* Device pointer to the int64 word count of the last encode (for async reads). */
+gtc_status gtc_local_count(const gtc_ctx* ctx, const int64_t** dev_k);
+
+/* Device pointer + length of rank `rank`'s message after the last exchange
+ * (world == 1: the local message; k is read back, waiting on the stream). */
+gtc_status gtc_message(gtc_ctx* ctx, int rank, const uint32_t** dev_words, int64_t* k);
+
+/* Wait for `stream`, then report and clear the sticky device flags:
+ * GTC_ENONFINITE, GTC_ECAPACITY, GTC_ECORRUPT or GTC_OK. */
+gtc_status gtc_check(gtc_ctx* ctx, cudaStream_t stream);
+
+/* Number of kernels libgtc launched on this context so far (NCCL's excluded). */
+int64_t gtc_kernel_launches(const gtc_ctx* ctx);
+
+const char* gtc_strerror(gtc_status status);
+const char* gtc_last_error_detail(const gtc_ctx* ctx);
+
+/* Destroy the NCCL communicator and host state; never frees caller memory. */
+void gtc_destroy(gtc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GTC_H */

@@ -1,0 +1,315 @@
+"""paper_1904_10584_b200 -- B200-native Gradient Threshold Compression (GTC).
+
+The hot path of the distributed trainer of arXiv 1904.10584, PAPER.md:222
+(Sec. VI-A): threshold-quantised gradient compression with residual
+accumulation, the all-to-all exchange of the sparse updates, their
+aggregation and the weight update.  All of it runs in libgtc.so
+(hand-written sm_100a CUDA + NCCL, C ABI in include/gtc.h).  This module is a
+thin ctypes binding with the same names as the C ABI (argument marshalling
+only) plus ``GTC``, a convenience wrapper that lets PyTorch own the device
+memory (workspace, tensors) and streams.
+
+There is no CPU fallback: if libgtc.so is missing or no CUDA device is
+present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgtc.so")
+
+GTC_OK = 0
+GTC_EINVAL = 1
+GTC_EDIM = 2
+GTC_EALIGN = 3
+GTC_ECUDA = 4
+GTC_ENCCL = 5
+GTC_ENONFINITE = 6
+GTC_ECORRUPT = 7
+GTC_ESTATE = 8
+GTC_ECAPACITY = 9
+GTC_EUNSUPPORTED = 10
+
+GTC_CMP_GT = 0
+GTC_CMP_GE = 1
+GTC_ACCUM_WEIGHTS = 0
+GTC_ACCUM_UPDATE = 1
+GTC_MAX_MSGS = 64
+GTC_TILE = 4096
+
+# every entry point of include/gtc.h: name -> (restype, argtypes)
+_vp, _i64, _i32, _u32, _f32, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                    ctypes.c_uint32, ctypes.c_float, ctypes.c_size_t)
+_SIGS = {
+    "gtc_get_unique_id": (_i32, [_vp]),
+    "gtc_init": (_i32, [ctypes.POINTER(_vp), _i64, _f32, _i32, _i32, _vp, _i32, _u32]),
+    "gtc_workspace_size": (_i32, [_vp, _i64, _i32, ctypes.POINTER(_sz)]),
+    "gtc_bind_workspace": (_i32, [_vp, _vp, _sz, _i64, _i32]),
+    "gtc_encode": (_i32, [_vp, _vp, _vp, _vp]),
+    "gtc_exchange": (_i32, [_vp, _vp]),
+    "gtc_decode_apply": (_i32, [_vp, _vp, _f32, _i32, _vp, _vp]),
+    "gtc_decode_apply_msgs": (_i32, [_vp, _vp, _vp, _i32, _vp, _f32, _i32, _vp, _vp]),
+    "gtc_last_counts": (_i32, [_vp, _vp]),
+    "gtc_local_count": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "gtc_message": (_i32, [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]),
+    "gtc_check": (_i32, [_vp, _vp]),
+    "gtc_kernel_launches": (_i64, [_vp]),
+    "gtc_strerror": (ctypes.c_char_p, [_i32]),
+    "gtc_last_error_detail": (ctypes.c_char_p, [_vp]),
+    "gtc_destroy": (None, [_vp]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libgtc.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class GTCError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        msg = load_library().gtc_strerror(status).decode()
+        super().__init__(f"{where}: {msg}" + (f" ({detail})" if detail else ""))
+        self.status = status
+
+
+def _chk(status: int, where: str, ctx=None, ok=(GTC_OK,)):
+    if status not in ok:
+        detail = load_library().gtc_last_error_detail(ctx).decode() if ctx else ""
+        raise GTCError(status, where, detail)
+    return status
+
+
+# ----------------------------------------------------------------- C-ABI names
+def gtc_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _chk(load_library().gtc_get_unique_id(buf), "gtc_get_unique_id")
+    return buf.raw
+
+
+def gtc_init(n_params: int, tau: float, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
+             cuda_device: int = 0, flags: int = GTC_CMP_GT):
+    ctx = _vp()
+    uid = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None
+    _chk(load_library().gtc_init(ctypes.byref(ctx), n_params, tau, rank, world, uid, cuda_device, flags),
+         "gtc_init")
+    return ctx
+
+
+def gtc_workspace_size(ctx, max_words_per_rank: int = 0, max_sim_msgs: int = 0) -> int:
+    out = _sz()
+    _chk(load_library().gtc_workspace_size(ctx, max_words_per_rank, max_sim_msgs, ctypes.byref(out)),
+         "gtc_workspace_size", ctx)
+    return out.value
+
+
+def gtc_bind_workspace(ctx, dev_ptr: int, nbytes: int, max_words_per_rank: int = 0, max_sim_msgs: int = 0):
+    _chk(load_library().gtc_bind_workspace(ctx, dev_ptr, nbytes, max_words_per_rank, max_sim_msgs),
+         "gtc_bind_workspace", ctx)
+
+
+def gtc_encode(ctx, grad_ptr: int | None, residual_ptr: int, stream: int):
+    _chk(load_library().gtc_encode(ctx, grad_ptr, residual_ptr, stream), "gtc_encode", ctx)
+
+
+def gtc_exchange(ctx, stream: int) -> int:
+    """Returns GTC_OK or GTC_ENONFINITE (exchange completed); raises otherwise."""
+    return _chk(load_library().gtc_exchange(ctx, stream), "gtc_exchange", ctx, ok=(GTC_OK, GTC_ENONFINITE))
+
+
+def gtc_decode_apply(ctx, target_ptr: int, alpha: float, mode: int, counts_out_ptr: int | None, stream: int):
+    _chk(load_library().gtc_decode_apply(ctx, target_ptr, alpha, mode, counts_out_ptr, stream),
+         "gtc_decode_apply", ctx)
+
+
+def gtc_decode_apply_msgs(ctx, msg_ptrs, counts, target_ptr: int, alpha: float, mode: int,
+                          counts_out_ptr: int | None, stream: int):
+    nm = len(msg_ptrs)
+    P = (_vp * max(nm, 1))(*msg_ptrs)
+    K = (_i64 * max(nm, 1))(*counts)
+    _chk(load_library().gtc_decode_apply_msgs(ctx, P, K, nm, target_ptr, alpha, mode, counts_out_ptr, stream),
+         "gtc_decode_apply_msgs", ctx)
+
+
+def gtc_last_counts(ctx, world: int):
+    buf = (_i64 * world)()
+    _chk(load_library().gtc_last_counts(ctx, buf), "gtc_last_counts", ctx)
+    return list(buf)
+
+
+def gtc_local_count(ctx) -> int:
+    p = _vp()
+    _chk(load_library().gtc_local_count(ctx, ctypes.byref(p)), "gtc_local_count", ctx)
+    return p.value
+
+
+def gtc_message(ctx, rank: int):
+    p, k = _vp(), _i64()
+    _chk(load_library().gtc_message(ctx, rank, ctypes.byref(p), ctypes.byref(k)), "gtc_message", ctx)
+    return p.value, k.value
+
+
+def gtc_check(ctx, stream: int) -> int:
+    return load_library().gtc_check(ctx, stream)
+
+
+def gtc_kernel_launches(ctx) -> int:
+    return load_library().gtc_kernel_launches(ctx)
+
+
+def gtc_strerror(status: int) -> str:
+    return load_library().gtc_strerror(status).decode()
+
+
+def gtc_last_error_detail(ctx) -> str:
+    return load_library().gtc_last_error_detail(ctx).decode()
+
+
+def gtc_destroy(ctx):
+    load_library().gtc_destroy(ctx)
+
+
+# ----------------------------------------------------------------- torch glue
+def _stream(stream, device):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def _ptr(t, name):
+    import torch
+
+    if t is None:
+        return None
+    if not (t.is_cuda and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous CUDA tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32")
+    return t.data_ptr()
+
+
+class GTC:
+    """One rank's GTC context with torch-owned workspace.
+
+    ``world > 1`` needs an initialised torch.distributed group (any backend)
+    to broadcast the 128-byte NCCL id from rank 0; the exchange itself runs on
+    libgtc's own NCCL communicator.
+    """
+
+    def __init__(self, n_params: int, tau: float, rank: int = 0, world: int = 1, device=None,
+                 cmp: str = "gt", max_words_per_rank: int = 0, max_sim_msgs: int = 0, group=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("GTC needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.n, self.tau, self.rank, self.world = int(n_params), float(tau), int(rank), int(world)
+        self.cmp = {"gt": GTC_CMP_GT, "ge": GTC_CMP_GE}[cmp]
+        uid = None
+        if world > 1:
+            import torch.distributed as dist
+
+            obj = [gtc_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = obj[0]
+        with torch.cuda.device(self.device):
+            self.ctx = gtc_init(self.n, self.tau, rank, world, uid, self.device.index, self.cmp)
+            nbytes = gtc_workspace_size(self.ctx, max_words_per_rank, max_sim_msgs)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            gtc_bind_workspace(self.ctx, self.workspace.data_ptr(), nbytes, max_words_per_rank, max_sim_msgs)
+
+    # --- the three calls of a step
+    def encode(self, grad, residual, stream=None):
+        if residual.numel() != self.n or (grad is not None and grad.numel() != self.n):
+            raise ValueError("grad/residual length != n_params")
+        gtc_encode(self.ctx, _ptr(grad, "grad"), _ptr(residual, "residual"), _stream(stream, self.device))
+
+    def exchange(self, stream=None) -> int:
+        return gtc_exchange(self.ctx, _stream(stream, self.device))
+
+    def decode_apply(self, target, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS, counts_out=None,
+                     stream=None):
+        import torch
+
+        if target.numel() != self.n:
+            raise ValueError("target length != n_params")
+        cptr = None
+        if counts_out is not None:
+            if counts_out.dtype != torch.int8 or counts_out.numel() != self.n or not counts_out.is_cuda:
+                raise ValueError("counts_out must be int8[n] on the device")
+            cptr = counts_out.data_ptr()
+        gtc_decode_apply(self.ctx, _ptr(target, "target"), alpha, mode, cptr, _stream(stream, self.device))
+
+    def step(self, grad, residual, target, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS, stream=None) -> int:
+        self.encode(grad, residual, stream)
+        st = self.exchange(stream)
+        self.decode_apply(target, alpha, mode, None, stream)
+        return st
+
+    # --- simulated workers / tests
+    def decode_apply_msgs(self, msgs, target, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS,
+                          counts_out=None, stream=None):
+        """msgs: list of (device int32/uint32 tensor or raw ptr, k)."""
+        ptrs, ks = [], []
+        for m in msgs:
+            if isinstance(m, tuple):
+                ptrs.append(m[0] if isinstance(m[0], int) else m[0].data_ptr())
+                ks.append(int(m[1]))
+            else:
+                ptrs.append(m.data_ptr())
+                ks.append(m.numel())
+        cptr = counts_out.data_ptr() if counts_out is not None else None
+        gtc_decode_apply_msgs(self.ctx, ptrs, ks, _ptr(target, "target"), alpha, mode, cptr,
+                              _stream(stream, self.device))
+
+    def message(self, rank: int | None = None):
+        """(device pointer, k) of a rank's message (local one when world == 1)."""
+        return gtc_message(self.ctx, self.rank if rank is None else rank)
+
+    def message_tensor(self, rank: int | None = None):
+        """The message as an int32 view into the workspace (bit pattern = uint32 words)."""
+        import torch
+
+        ptr, k = self.message(rank)
+        off = ptr - self.workspace.data_ptr()
+        return self.workspace[off: off + 4 * k].view(torch.int32)
+
+    def local_count_tensor(self):
+        import torch
+
+        off = gtc_local_count(self.ctx) - self.workspace.data_ptr()
+        return self.workspace[off: off + 8].view(torch.int64)
+
+    def last_counts(self):
+        return gtc_last_counts(self.ctx, self.world)
+
+    def check(self, stream=None) -> int:
+        return gtc_check(self.ctx, _stream(stream, self.device))
+
+    def kernel_launches(self) -> int:
+        return gtc_kernel_launches(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            gtc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
