@@ -183,6 +183,18 @@ def gtc_destroy(ctx):
 
 
 # ----------------------------------------------------------------- torch glue
+def broadcast_unique_id(rank: int, group=None) -> bytes:
+    """Rank 0 creates the 128-byte NCCL id; every rank of ``group`` (an
+    initialised torch.distributed group, any backend) receives the same bytes."""
+    import torch.distributed as dist
+
+    obj = [gtc_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if not (isinstance(obj[0], bytes) and len(obj[0]) == 128):
+        raise RuntimeError("NCCL unique id broadcast failed")
+    return obj[0]
+
+
 def _stream(stream, device):
     import torch
 
@@ -221,11 +233,7 @@ class GTC:
         self.cmp = {"gt": GTC_CMP_GT, "ge": GTC_CMP_GE}[cmp]
         uid = None
         if world > 1:
-            import torch.distributed as dist
-
-            obj = [gtc_get_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0, group=group)
-            uid = obj[0]
+            uid = broadcast_unique_id(rank, group)
         with torch.cuda.device(self.device):
             self.ctx = gtc_init(self.n, self.tau, rank, world, uid, self.device.index, self.cmp)
             nbytes = gtc_workspace_size(self.ctx, max_words_per_rank, max_sim_msgs)

@@ -1,0 +1,38 @@
+"""Multi-GPU parity through NCCL (torchrun, one process per GPU)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ngpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("cmp", ["gt", "ge"])
+def test_nccl_exchange_parity(world, cmp):
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, GTC_CMP=cmp, GTC_STEPS="4", GTC_N="1000003")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MULTIGPU OK" in p.stdout
+
+
+def test_nccl_exchange_lstm_am_size():
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="2", GTC_N="24286575")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29532", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
