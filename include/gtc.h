@@ -148,6 +148,13 @@ gtc_status gtc_exchange(gtc_ctx* ctx, cudaStream_t stream);
 gtc_status gtc_decode_apply(gtc_ctx* ctx, float* target, float alpha, int mode,
                             int8_t* counts_out, cudaStream_t stream);
 
+/* One whole step: gtc_encode, gtc_exchange, gtc_decode_apply in one call
+ * (same arguments and semantics; returns the first failing status, or
+ * GTC_ENONFINITE from the exchange after completing the step).  Saves the
+ * per-call overhead of three calls on launch-bound sizes. */
+gtc_status gtc_step(gtc_ctx* ctx, const float* grad, float* residual, float* target, float alpha,
+                    int mode, cudaStream_t stream);
+
 /* Same aggregate+apply over caller-supplied messages, no NCCL: used for
  * simulated workers on one GPU and for tests.
  *  msgs   : host array of nmsg DEVICE pointers to uint32 words (ascending)

@@ -50,6 +50,7 @@ _SIGS = {
     "gtc_encode": (_i32, [_vp, _vp, _vp, _vp]),
     "gtc_exchange": (_i32, [_vp, _vp]),
     "gtc_decode_apply": (_i32, [_vp, _vp, _f32, _i32, _vp, _vp]),
+    "gtc_step": (_i32, [_vp, _vp, _vp, _vp, _f32, _i32, _vp]),
     "gtc_decode_apply_msgs": (_i32, [_vp, _vp, _vp, _i32, _vp, _f32, _i32, _vp, _vp]),
     "gtc_last_counts": (_i32, [_vp, _vp]),
     "gtc_local_count": (_i32, [_vp, ctypes.POINTER(_vp)]),
@@ -133,6 +134,13 @@ def gtc_exchange(ctx, stream: int) -> int:
 def gtc_decode_apply(ctx, target_ptr: int, alpha: float, mode: int, counts_out_ptr: int | None, stream: int):
     _chk(load_library().gtc_decode_apply(ctx, target_ptr, alpha, mode, counts_out_ptr, stream),
          "gtc_decode_apply", ctx)
+
+
+def gtc_step(ctx, grad_ptr: int | None, residual_ptr: int, target_ptr: int, alpha: float, mode: int,
+             stream: int) -> int:
+    """encode + exchange + decode_apply; returns GTC_OK or GTC_ENONFINITE."""
+    return _chk(load_library().gtc_step(ctx, grad_ptr, residual_ptr, target_ptr, alpha, mode, stream),
+                "gtc_step", ctx, ok=(GTC_OK, GTC_ENONFINITE))
 
 
 def gtc_decode_apply_msgs(ctx, msg_ptrs, counts, target_ptr: int, alpha: float, mode: int,
@@ -263,10 +271,33 @@ class GTC:
         gtc_decode_apply(self.ctx, _ptr(target, "target"), alpha, mode, cptr, _stream(stream, self.device))
 
     def step(self, grad, residual, target, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS, stream=None) -> int:
-        self.encode(grad, residual, stream)
-        st = self.exchange(stream)
-        self.decode_apply(target, alpha, mode, None, stream)
-        return st
+        """encode -> exchange -> decode_apply in one C call."""
+        for t, name in ((residual, "residual"), (target, "target")):
+            if t.numel() != self.n:
+                raise ValueError(f"{name} length != n_params")
+        if grad is not None and grad.numel() != self.n:
+            raise ValueError("grad length != n_params")
+        return gtc_step(self.ctx, _ptr(grad, "grad"), _ptr(residual, "residual"), _ptr(target, "target"),
+                        alpha, mode, _stream(stream, self.device))
+
+    def stepper(self, grads, residual, target, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS, stream=None):
+        """A validated-once step closure for hot loops: ``f(i)`` runs one step
+        on ``grads[i % len(grads)]`` with a single ctypes call."""
+        for t in list(grads) + [residual, target]:
+            _ptr(t, "tensor")
+            if t.numel() != self.n:
+                raise ValueError("tensor length != n_params")
+        fn = load_library().gtc_step
+        ctx, gp = self.ctx, [g.data_ptr() for g in grads]
+        rp, tp, sp = residual.data_ptr(), target.data_ptr(), _stream(stream, self.device)
+        ng, a, m = len(gp), float(alpha), int(mode)
+
+        def f(i):
+            st = fn(ctx, gp[i % ng], rp, tp, a, m, sp)
+            if st != GTC_OK and st != GTC_ENONFINITE:
+                _chk(st, "gtc_step", ctx)
+            return st
+        return f
 
     # --- simulated workers / tests
     def decode_apply_msgs(self, msgs, target, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS,

@@ -1,45 +1,86 @@
 // encode.cu -- fused GTC encode for sm_100a (Sec. VI-A, steps 1-4).
 //
-// One pass over the parameter vector, HBM-bound (no contraction, no tensor
-// cores).  Per element i (fp32, RNE, no FTZ):
+// Per element i (fp32, RNE, no FTZ):
 //     v = r[i] + g[i]                               residual accumulation
-//     sel = |v| > tau   (GT)   /   |v| >= tau  (GE)  threshold
-//     r[i] = sel ? v -+ tau : v                      one +-tau quantum leaves
-//     word = (i << 1) | (v < 0)                      32-bit packing
-// and the selected words are compacted, in ascending index order, into the
-// message with a single-pass decoupled look-back scan:
-//   - a CTA takes a dynamic ticket (= tile id, so every predecessor tile is
-//     already resident: look-back cannot deadlock),
-//   - 128-bit streaming loads of g and r (8 outstanding per thread),
-//   - per-(round, warp) word counts from three __ballot_sync/__popc (a thread
-//     holds <= 4 words per round), one 32-entry warp scan for the tile,
-//   - warp 0 publishes the tile aggregate, sums predecessors' descriptors 32 at
-//     a time until it meets an inclusive prefix, publishes its own prefix,
-//   - the words are staged in shared memory and written out coalesced.
-// Descriptors carry a per-call epoch, so no memset is needed between calls;
-// the ticket counter of the next call is reset by tile 0 of this one.
+//     sel = |v| > tau   (GT)   /   |v| >= tau  (GE)  threshold (DESIGN R1)
+//     r[i] = sel ? v -+ tau : v                      one +-tau quantum leaves (R2)
+//     word = (i << 1) | (v < 0)                      32-bit packing (R3)
+// and the selected words are compacted, in ascending index order (R4), into
+// one contiguous message.  HBM-bound: no contraction, no tensor cores.
+//
+// Kernel 1, gtc_encode_tiles_kernel (the streaming pass, ~all of the bytes):
+//   - persistent, 2 CTAs x 256 threads per SM; CTA b owns a contiguous chunk
+//     of tiles (kTile = 4096 params each): no CTA ever waits for another, so
+//     there is no residency requirement and no look-back chain;
+//   - thread 0 keeps kStages tiles in flight with 1-D TMA bulk copies
+//     (cp.async.bulk.shared::cluster.global.mbarrier::complete_tx) of r and g
+//     into shared memory; the CTA reads its stage with conflict-free 128-bit
+//     LDS and writes r back with 128-bit coalesced stores (L1::no_allocate);
+//   - element order inside a tile is (round j, warp, lane, component) =
+//     ascending index; intra-tile ranks come from three __ballot_sync/__popc
+//     per round (a thread holds <= 4 words per round) and one 32-entry warp
+//     scan over the (round, warp) totals;
+//   - the tile's words go, compacted, to its slot of a tile-major scratch; its
+//     count to tile_cnt[]; the chunk's count to chunk_sum[b] at the end.
+// Kernel 2, gtc_compact_kernel (reads/writes ~8*rho B/param): one warp per
+//   tile; a CTA sums the chunk sums of earlier chunks and the counts of the
+//   earlier tiles of its chunk (all loads independent), derives its tiles'
+//   global offsets and copies the words into the message.
+// Every count is rewritten every call: no atomics, no memset, no host state
+// (the pair is CUDA-graph capturable).
 //
 // HBM bytes per parameter (algorithmic): 4 (read g) + 4 (read r) + 4 (write r)
-// + 4*rho (write words) + 4/kTile (tile offset).
+// + 4*rho (write words); + 4 B per tile (offsets).  The scratch round trip
+// adds 8*rho (0.08 B/param at rho = 1 %).
 #include "gtc_internal.cuh"
+
+#include <mutex>
 
 namespace gtc {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kStages = 3;                       // TMA pipeline depth per CTA
+constexpr int kTileBytes = kTile * 4;             // 16 KB per tensor per tile
+constexpr int kVec4PerTile = kTile / 4;           // float4 per tensor per tile
+constexpr int kCompactThreads = 256;
 
-__device__ __forceinline__ float4 ld_stream_nc(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = smem_addr(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    }
+}
+
+// 1-D bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
 
 __device__ __forceinline__ void st_stream(float4* p, const float4& v) {
@@ -47,24 +88,10 @@ __device__ __forceinline__ void st_stream(float4* p, const float4& v) {
                  :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
-}
-
-__device__ __forceinline__ unsigned long long make_desc(unsigned epoch, unsigned status, unsigned value) {
-    return ((unsigned long long)((epoch << 2) | status) << 32) | value;
 }
 
 __device__ __forceinline__ float comp(const float4& v, int e) {
@@ -74,216 +101,269 @@ __device__ __forceinline__ void set_comp(float4& v, int e, float x) {
     if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
 }
 
-__device__ __forceinline__ unsigned warp_sum(unsigned x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
-    return x;
-}
+template <bool HAS_G>
+struct Smem {
+    float4 r[kStages][kVec4PerTile];
+    float4 g[HAS_G ? kStages : 1][HAS_G ? kVec4PerTile : 1];
+};
 
-// Warp 0: publish this tile's aggregate, look back for the exclusive prefix,
-// publish the inclusive prefix.  Returns the exclusive prefix (all lanes).
-__device__ __forceinline__ unsigned look_back(const EncodeParams& p, unsigned ep, unsigned tile,
-                                              unsigned total, int lane) {
-    if (tile == 0) {
-        if (lane == 0) st_relaxed_u64(&p.desc[0], make_desc(ep, kDescPrefix, total));
-        return 0u;
-    }
-    if (lane == 0) st_relaxed_u64(&p.desc[tile], make_desc(ep, kDescAggregate, total));
-    const unsigned tag_agg = (ep << 2) | kDescAggregate;
-    const unsigned tag_pre = (ep << 2) | kDescPrefix;
-    unsigned excl = 0;
-    long long pred = (long long)tile - 1;
-    while (true) {
-        const long long t = pred - lane;  // lane 0 = nearest predecessor
-        unsigned long long d = 0;
-        bool ok = false;
-        while (true) {
-            if (!ok) {
-                d = (t >= 0) ? ld_relaxed_u64(&p.desc[t]) : make_desc(ep, kDescPrefix, 0u);
-                const unsigned tag = (unsigned)(d >> 32);
-                ok = (tag == tag_agg) || (tag == tag_pre);
-            }
-            if (__all_sync(kFull, ok)) break;
-        }
-        const bool is_pre = ((unsigned)(d >> 32)) == tag_pre;
-        const unsigned pm = __ballot_sync(kFull, is_pre);
-        unsigned val = (unsigned)d;
-        if (pm) {
-            const int first = __ffs(pm) - 1;
-            excl += warp_sum(lane <= first ? val : 0u);
-            break;
-        }
-        excl += warp_sum(val);
-        pred -= 32;
-    }
-    if (lane == 0) st_relaxed_u64(&p.desc[tile], make_desc(ep, kDescPrefix, excl + total));
-    return excl;
+// Thread 0: start the TMA copies of `tile` into stage s (full tiles only; the
+// ragged last tile is loaded directly by the consumer).
+template <bool HAS_G>
+__device__ __forceinline__ void issue_stage(const EncodeParams& p, Smem<HAS_G>& sm, unsigned long long* full,
+                                            int s, long long tile) {
+    if (tile >= p.num_tiles) return;
+    const long long base = tile * kTile;
+    if (base + kTile > p.n) return;
+    mbar_arrive_expect_tx(&full[s], HAS_G ? 2u * kTileBytes : (unsigned)kTileBytes);
+    tma_load_1d(sm.r[s], p.r + base, kTileBytes, &full[s]);
+    if (HAS_G) tma_load_1d(sm.g[s], p.g + base, kTileBytes, &full[s]);
 }
 
 template <int CMP, bool HAS_G>
-__global__ void __launch_bounds__(kEncThreads, 4) gtc_encode_kernel(const EncodeParams p) {
-    __shared__ unsigned s_words[kTile];          // staged message words of this tile
+__global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const EncodeParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem<HAS_G>& sm = *reinterpret_cast<Smem<HAS_G>*>(smem_raw);
+    __shared__ __align__(8) unsigned long long full[kStages];
     __shared__ unsigned s_scan[kEncVec * kEncWarps];
-    __shared__ unsigned s_tile, s_epoch, s_excl, s_total;
+    __shared__ unsigned s_total;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
+    const long long t_begin = (long long)blockIdx.x * p.chunk_tiles;
+    const long long t_end = min(t_begin + p.chunk_tiles, (long long)p.num_tiles);
 
     if (tid == 0) {
-        // The ticket address depends on the epoch just read, so the ticket is
-        // taken after the read; the last tile advances the epoch only after
-        // every other tile has published (hence read it): one launch sees one epoch.
-        const unsigned ep = *reinterpret_cast<volatile unsigned*>(&p.ctrl->epoch);
-        const unsigned t = atomicAdd(&p.ctrl->ticket[ep & 1u], 1u);
-        if (t == 0) p.ctrl->ticket[(ep + 1u) & 1u] = 0u;
-        s_tile = t;
-        s_epoch = ep;
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+        for (int s = 0; s < kStages; ++s)
+            if (t_begin + s < t_end) issue_stage<HAS_G>(p, sm, full, s, t_begin + s);
     }
     __syncthreads();
-    const unsigned tile = s_tile;
-    const long long base = (long long)tile * kTile;
-    const bool full = base + kTile <= p.n;
-
-    // ---- load: r (and g) for kEncVec rounds, all loads issued before use
-    float4 rv[kEncVec];
-    float4 gv[kEncVec];
-    if (full) {
-        const float4* r4 = reinterpret_cast<const float4*>(p.r + base);
-#pragma unroll
-        for (int j = 0; j < kEncVec; ++j) rv[j] = ld_stream(r4 + j * kEncThreads + tid);
-        if (HAS_G) {
-            const float4* g4 = reinterpret_cast<const float4*>(p.g + base);
-#pragma unroll
-            for (int j = 0; j < kEncVec; ++j) gv[j] = ld_stream_nc(g4 + j * kEncThreads + tid);
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < kEncVec; ++j) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const long long i = base + (long long)(j * kEncThreads + tid) * 4 + e;
-                set_comp(rv[j], e, i < p.n ? p.r[i] : 0.0f);
-                if (HAS_G) set_comp(gv[j], e, i < p.n ? p.g[i] : 0.0f);
-            }
-        }
-    }
-
-    // ---- residual accumulate, threshold, quantize (R1, R2)
     const float tau = p.tau;
-    unsigned sel = 0u, neg = 0u;
-    bool nonfinite = false;
-#pragma unroll
-    for (int j = 0; j < kEncVec; ++j) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float v = HAS_G ? __fadd_rn(comp(rv[j], e), comp(gv[j], e)) : comp(rv[j], e);
-            const float a = fabsf(v);
-            nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
-            const bool s = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
-            const bool ng = v < 0.0f;
-            const float rn = s ? (ng ? __fadd_rn(v, tau) : __fsub_rn(v, tau)) : v;
-            set_comp(rv[j], e, rn);
-            sel |= (unsigned)s << (j * 4 + e);
-            neg |= (unsigned)(s && ng) << (j * 4 + e);
-        }
-    }
+    const unsigned lt = lanemask_lt();
+    unsigned chunk_total = 0;  // meaningful in warp 0, lane 31
 
-    // ---- write the residual back
-    if (full) {
-        float4* r4 = reinterpret_cast<float4*>(p.r + base);
+    int it = 0;
+    for (long long tile = t_begin; tile < t_end; ++tile, ++it) {
+        const int s = it % kStages;
+        const long long base = tile * kTile;
+        const bool full_tile = base + kTile <= p.n;
+
+        // ---- load the tile from its stage (or directly, for the ragged tail)
+        float4 rv[kEncVec];
+        float4 gv[kEncVec];
+        if (full_tile) {
+            mbar_wait(&full[s], (unsigned)(it / kStages) & 1u);
 #pragma unroll
-        for (int j = 0; j < kEncVec; ++j) st_stream(r4 + j * kEncThreads + tid, rv[j]);
-    } else {
+            for (int j = 0; j < kEncVec; ++j) {
+                rv[j] = sm.r[s][j * kEncThreads + tid];
+                if (HAS_G) gv[j] = sm.g[s][j * kEncThreads + tid];
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kEncVec; ++j) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const long long i = base + (long long)(j * kEncThreads + tid) * 4 + e;
+                    set_comp(rv[j], e, i < p.n ? p.r[i] : 0.0f);
+                    if (HAS_G) set_comp(gv[j], e, i < p.n ? p.g[i] : 0.0f);
+                }
+            }
+        }
+
+        // ---- residual accumulate, threshold, quantize
+        unsigned sel = 0u, neg = 0u;
+        bool nonfinite = false;
 #pragma unroll
         for (int j = 0; j < kEncVec; ++j) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const long long i = base + (long long)(j * kEncThreads + tid) * 4 + e;
-                if (i < p.n) p.r[i] = comp(rv[j], e);
+                const float v = HAS_G ? __fadd_rn(comp(rv[j], e), comp(gv[j], e)) : comp(rv[j], e);
+                const float a = fabsf(v);
+                nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
+                const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
+                const bool ng = v < 0.0f;
+                const float rn = sl ? (ng ? __fadd_rn(v, tau) : __fsub_rn(v, tau)) : v;
+                set_comp(rv[j], e, rn);
+                sel |= (unsigned)sl << (j * 4 + e);
+                neg |= (unsigned)(sl && ng) << (j * 4 + e);
+            }
+        }
+
+        // ---- write the residual back
+        if (full_tile) {
+            float4* r4 = reinterpret_cast<float4*>(p.r + base);
+#pragma unroll
+            for (int j = 0; j < kEncVec; ++j) st_stream(r4 + j * kEncThreads + tid, rv[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kEncVec; ++j) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const long long i = base + (long long)(j * kEncThreads + tid) * 4 + e;
+                    if (i < p.n) p.r[i] = comp(rv[j], e);
+                }
+            }
+        }
+        if (__any_sync(kFull, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
+
+        // ---- intra-tile ranks
+        unsigned my_off[kEncVec];
+#pragma unroll
+        for (int j = 0; j < kEncVec; ++j) {
+            const unsigned c = __popc((sel >> (4 * j)) & 0xfu);  // 0..4
+            const unsigned b0 = __ballot_sync(kFull, c & 1u);
+            const unsigned b1 = __ballot_sync(kFull, c & 2u);
+            const unsigned b2 = __ballot_sync(kFull, c & 4u);
+            my_off[j] = __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+            if (lane == 0) s_scan[j * kEncWarps + warp] = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+        }
+        __syncthreads();  // stage s fully read; s_scan complete
+
+        if (warp == 0) {
+            if (lane == 0 && tile + kStages < t_end)
+                issue_stage<HAS_G>(p, sm, full, s, tile + kStages);  // refill stage s
+            const unsigned x = s_scan[lane];
+            unsigned incl = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            s_scan[lane] = incl - x;
+            if (lane == 31) {
+                s_total = incl;
+                p.tile_cnt[tile] = (int)incl;
+                chunk_total += incl;
+            }
+        }
+        __syncthreads();  // tile-local offsets known
+
+        // ---- pack and store the words, compacted, in the tile's scratch slot
+        if (s_total != 0) {
+            unsigned* dst = p.scratch + base;
+#pragma unroll
+            for (int j = 0; j < kEncVec; ++j) {
+                unsigned o = s_scan[j * kEncWarps + warp] + my_off[j];
+                const unsigned i0 = (unsigned)(base + (long long)(j * kEncThreads + tid) * 4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if ((sel >> (4 * j + e)) & 1u) {
+                        dst[o] = ((i0 + e) << 1) | ((neg >> (4 * j + e)) & 1u);
+                        ++o;
+                    }
+                }
             }
         }
     }
-    if (__any_sync(kFull, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
+    if (tid == 31) p.chunk_sum[blockIdx.x] = chunk_total;
+}
 
-    // ---- intra-tile ranks: element order is (round j, warp, lane, e)
-    const unsigned lt = lanemask_lt();
-    unsigned my_off[kEncVec];
+// Kernel 2: one warp per tile, kCompactWarps tiles per CTA.
+constexpr int kCompactWarps = kCompactThreads / 32;
+
+__global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const EncodeParams p) {
+    __shared__ unsigned s_red[kCompactWarps];
+    __shared__ unsigned s_cnt[kCompactWarps];
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int t_cta = blockIdx.x * kCompactWarps;      // first tile of this CTA
+    const int c = t_cta / p.chunk_tiles;               // its kernel-1 chunk
+    const int t_chunk = c * p.chunk_tiles;             // first tile of that chunk
+    const int tile = t_cta + warp;
+    const bool has_tile = tile < p.num_tiles;
+
+    // words before this CTA: earlier chunks + earlier tiles of its chunk
+    unsigned part = 0;
+    for (int i = tid; i < c; i += kCompactThreads) part += __ldcg(p.chunk_sum + i);
+    for (int i = t_chunk + tid; i < t_cta; i += kCompactThreads) part += (unsigned)__ldcg(p.tile_cnt + i);
+    const unsigned my_cnt = has_tile ? (unsigned)__ldcg(p.tile_cnt + tile) : 0u;
 #pragma unroll
-    for (int j = 0; j < kEncVec; ++j) {
-        const unsigned c = __popc((sel >> (4 * j)) & 0xfu);  // 0..4
-        const unsigned b0 = __ballot_sync(kFull, c & 1u);
-        const unsigned b1 = __ballot_sync(kFull, c & 2u);
-        const unsigned b2 = __ballot_sync(kFull, c & 4u);
-        my_off[j] = __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
-        if (lane == 0) s_scan[j * kEncWarps + warp] = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+    if (lane == 0) {
+        s_red[warp] = part;
+        s_cnt[warp] = my_cnt;
     }
     __syncthreads();
-
-    if (warp == 0) {
-        const unsigned x = s_scan[lane];
-        unsigned incl = x;
+    if (!has_tile) return;
+    unsigned prefix = 0, before = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-        }
-        s_scan[lane] = incl - x;
-        const unsigned total = __shfl_sync(kFull, incl, 31);
-        const unsigned excl = look_back(p, s_epoch, tile, total, lane);
-        if (lane == 0) {
-            s_excl = excl;
-            s_total = total;
-            p.tile_off[tile] = (int)excl;
-            if ((int)tile == p.num_tiles - 1) {
-                p.ctrl->epoch = s_epoch >= kEpochMax ? 1u : s_epoch + 1u;
-                const unsigned k = excl + total;
-                p.tile_off[p.num_tiles] = (int)k;
-                p.ctrl->k = (long long)k;
-                if ((long long)k > p.capacity) atomicOr(&p.ctrl->flags, kFlagCapacity);
-            }
+    for (int w = 0; w < kCompactWarps; ++w) {
+        prefix += s_red[w];
+        before += (w < warp) ? s_cnt[w] : 0u;
+    }
+    const long long dst0 = (long long)prefix + before;
+
+    if (lane == 0) {
+        p.tile_off[tile] = (int)dst0;
+        if (tile == p.num_tiles - 1) {
+            const long long k = dst0 + my_cnt;
+            p.tile_off[p.num_tiles] = (int)k;
+            p.ctrl->k = k;
+            if (k > p.capacity) atomicOr(&p.ctrl->flags, kFlagCapacity);
         }
     }
-    __syncthreads();
-
-    // ---- pack (R3) into shared memory at each word's rank within the tile
+    const unsigned* src = p.scratch + (long long)tile * kTile;
+    for (unsigned j0 = 0; j0 < my_cnt; j0 += 4 * 32) {
+        unsigned w[4];
 #pragma unroll
-    for (int j = 0; j < kEncVec; ++j) {
-        unsigned o = s_scan[j * kEncWarps + warp] + my_off[j];
-        const unsigned i0 = (unsigned)(base + (long long)(j * kEncThreads + tid) * 4);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if ((sel >> (4 * j + e)) & 1u) {
-                s_words[o] = ((i0 + e) << 1) | ((neg >> (4 * j + e)) & 1u);
-                ++o;
-            }
+        for (int u = 0; u < 4; ++u) {
+            const unsigned j = j0 + u * 32 + lane;
+            if (j < my_cnt) w[u] = __ldcg(src + j);
         }
-    }
-    __syncthreads();
-
-    // ---- coalesced copy of the tile's words to its slice of the message
-    const unsigned total = s_total;
-    const long long excl = s_excl;
-    for (unsigned i = tid; i < total; i += kEncThreads) {
-        const long long pos = excl + i;
-        if (pos < p.capacity) p.words[pos] = s_words[i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned j = j0 + u * 32 + lane;
+            if (j < my_cnt && dst0 + j < p.capacity) p.words[dst0 + j] = w[u];
+        }
     }
 }
 
-template <int CMP>
-cudaError_t launch_cmp(const EncodeParams& p, cudaStream_t s) {
-    if (p.num_tiles == 0) return cudaSuccess;
-    if (p.g)
-        gtc_encode_kernel<CMP, true><<<p.num_tiles, kEncThreads, 0, s>>>(p);
-    else
-        gtc_encode_kernel<CMP, false><<<p.num_tiles, kEncThreads, 0, s>>>(p);
+template <int CMP, bool HAS_G>
+cudaError_t launch_tiles(EncodeParams& p, cudaStream_t s) {
+    static std::once_flag once;
+    static int per_sm = 0, sms = 0;
+    static cudaError_t init_err = cudaSuccess;
+    const size_t smem = sizeof(Smem<HAS_G>);
+    auto kern = gtc_encode_tiles_kernel<CMP, HAS_G>;
+    std::call_once(once, [&] {
+        init_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (init_err != cudaSuccess) return;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        init_err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (init_err != cudaSuccess) return;
+        init_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEncThreads, smem);
+        if (per_sm < 1) per_sm = 1;
+    });
+    if (init_err != cudaSuccess) return init_err;
+    int grid = sms * per_sm;
+    if (grid > kMaxChunks) grid = kMaxChunks;
+    if (grid > p.num_tiles) grid = p.num_tiles;
+    p.chunk_tiles = (p.num_tiles + grid - 1) / grid;
+    p.num_chunks = (p.num_tiles + p.chunk_tiles - 1) / p.chunk_tiles;
+    kern<<<p.num_chunks, kEncThreads, smem, s>>>(p);
     return cudaGetLastError();
+}
+
+template <int CMP>
+cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
+    return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
 }
 
 }  // namespace
 
-cudaError_t launch_encode(const EncodeParams& p, int cmp_mode, cudaStream_t s) {
-    return cmp_mode == GTC_CMP_GE ? launch_cmp<GTC_CMP_GE>(p, s) : launch_cmp<GTC_CMP_GT>(p, s);
+cudaError_t launch_encode(const EncodeParams& p_in, int cmp_mode, cudaStream_t s) {
+    if (p_in.num_tiles == 0) return cudaSuccess;
+    EncodeParams p = p_in;
+    cudaError_t e = cmp_mode == GTC_CMP_GE ? launch_cmp<GTC_CMP_GE>(p, s) : launch_cmp<GTC_CMP_GT>(p, s);
+    if (e != cudaSuccess) return e;
+    gtc_compact_kernel<<<(p.num_tiles + kCompactWarps - 1) / kCompactWarps, kCompactThreads, 0, s>>>(p);
+    return cudaGetLastError();
 }
 
 }  // namespace gtc

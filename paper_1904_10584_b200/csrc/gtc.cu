@@ -23,16 +23,18 @@ enum class Stage { kBound, kEncoded, kExchanged };
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the bound base, each 256-byte aligned):
-//   ctrl      Ctrl                              k, flags, tickets
-//   desc      u64[num_tiles]                    look-back descriptors
+//   ctrl      Ctrl                              k, flags
+//   chunk_sum u32[kMaxChunks]                   words per encode-kernel-1 chunk
+//   tile_cnt  i32[num_tiles]                    words per tile
 //   tile_off  i32[num_tiles + 1]                this rank's tile offsets
+//   scratch   u32[num_tiles * kTile]            tile-major words (encode kernel 1)
 //   send      u32[capacity]                     this rank's message
 //   kx_all    i64[2 * world]                    all-gathered (k, flags)   (world > 1)
 //   recv      u32[world * capacity]             all-gathered messages     (world > 1)
 //   recv_off  i32[world * (num_tiles + 1)]      all-gathered tile offsets (world > 1)
 //   sim_off   i32[max_sim_msgs * (num_tiles+1)] tile offsets for decode_apply_msgs
 struct Layout {
-    size_t ctrl, desc, tile_off, send, kx_all, recv, recv_off, sim_off, total;
+    size_t ctrl, chunk_sum, tile_cnt, tile_off, scratch, send, kx_all, recv, recv_off, sim_off, total;
 };
 
 Layout make_layout(long long n, int world, long long capacity, int max_sim_msgs) {
@@ -40,8 +42,10 @@ Layout make_layout(long long n, int world, long long capacity, int max_sim_msgs)
     Layout L{};
     size_t o = 0;
     L.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
-    L.desc = o;      o = align_up(o + sizeof(unsigned long long) * (size_t)std::max(tiles, 1LL), 256);
+    L.chunk_sum = o; o = align_up(o + sizeof(unsigned) * (size_t)kMaxChunks, 256);
+    L.tile_cnt = o;  o = align_up(o + sizeof(int) * (size_t)std::max(tiles, 1LL), 256);
     L.tile_off = o;  o = align_up(o + sizeof(int) * (size_t)(tiles + 1), 256);
+    L.scratch = o;   o = align_up(o + sizeof(unsigned) * (size_t)std::max(tiles, 1LL) * kTile, 256);
     L.send = o;      o = align_up(o + sizeof(unsigned) * (size_t)std::max(capacity, 1LL), 256);
     if (world > 1) {
         L.kx_all = o;   o = align_up(o + sizeof(long long) * 2 * (size_t)world, 256);
@@ -72,8 +76,10 @@ struct gtc_ctx {
     Layout L{};
 
     Ctrl* ctrl = nullptr;
-    unsigned long long* desc = nullptr;
+    unsigned* chunk_sum = nullptr;
+    int* tile_cnt = nullptr;
     int* tile_off = nullptr;
+    unsigned* scratch = nullptr;
     unsigned* send = nullptr;
     long long* kx_all = nullptr;
     unsigned* recv = nullptr;
@@ -220,14 +226,9 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     if (bytes < L.total) return fail(c, GTC_EINVAL, "workspace too small");
     DeviceGuard g(c->device);
     unsigned char* b = static_cast<unsigned char*>(dev_ptr);
-    // Control block, descriptors (epoch 0 = never valid) and offsets start at 0;
-    // the first encode runs with epoch 1.
-    cudaError_t e = cudaMemset(b, 0, L.send);
+    // Control block, chunk sums, counts and offsets start at 0.
+    cudaError_t e = cudaMemset(b, 0, L.scratch);
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: cudaMemset");
-    const unsigned first_epoch = 1u;
-    e = cudaMemcpy(&reinterpret_cast<Ctrl*>(b + L.ctrl)->epoch, &first_epoch, sizeof(first_epoch),
-                   cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(c, e, "bind: epoch");
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: sync");
     c->ws = b;
@@ -236,8 +237,10 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     c->max_sim_msgs = max_sim_msgs;
     c->L = L;
     c->ctrl = reinterpret_cast<Ctrl*>(b + L.ctrl);
-    c->desc = reinterpret_cast<unsigned long long*>(b + L.desc);
+    c->chunk_sum = reinterpret_cast<unsigned*>(b + L.chunk_sum);
+    c->tile_cnt = reinterpret_cast<int*>(b + L.tile_cnt);
     c->tile_off = reinterpret_cast<int*>(b + L.tile_off);
+    c->scratch = reinterpret_cast<unsigned*>(b + L.scratch);
     c->send = reinterpret_cast<unsigned*>(b + L.send);
     if (c->world > 1) {
         c->kx_all = reinterpret_cast<long long*>(b + L.kx_all);
@@ -272,13 +275,15 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     p.tau = c->tau;
     p.words = c->send;
     p.capacity = c->capacity;
-    p.desc = c->desc;
+    p.scratch = c->scratch;
+    p.tile_cnt = c->tile_cnt;
+    p.chunk_sum = c->chunk_sum;
     p.tile_off = c->tile_off;
     p.ctrl = c->ctrl;
     p.num_tiles = c->num_tiles;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "encode: launch");
-    c->launches += 1;
+    c->launches += 2;
     c->stage = Stage::kEncoded;
     return GTC_OK;
 }
@@ -372,6 +377,16 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     if (c->num_tiles > 0) c->launches += 1;
     c->stage = Stage::kBound;
     return GTC_OK;
+}
+
+gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha, int mode,
+                    cudaStream_t stream) {
+    gtc_status s = gtc_encode(c, grad, residual, stream);
+    if (s != GTC_OK) return s;
+    const gtc_status sx = gtc_exchange(c, stream);
+    if (sx != GTC_OK && sx != GTC_ENONFINITE) return sx;
+    s = gtc_decode_apply(c, target, alpha, mode, nullptr, stream);
+    return s != GTC_OK ? s : sx;
 }
 
 gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const int64_t* counts, int nmsg,

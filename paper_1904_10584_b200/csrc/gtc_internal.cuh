@@ -11,10 +11,11 @@
 namespace gtc {
 
 constexpr int kTile = GTC_TILE;                        // parameters per tile
-constexpr int kEncThreads = 256;                       // encode CTA size
+constexpr int kEncThreads = 512;                       // encode CTA size
 constexpr int kEncWarps = kEncThreads / 32;
 constexpr int kEncVec = kTile / (kEncThreads * 4);     // float4 per thread per tensor
 constexpr int kDecThreads = 256;                       // decode_apply CTA size
+constexpr int kDecMaxTilesPerCta = 8;                  // <= 32 KB of int8 counts per CTA
 static_assert(kEncVec * kEncWarps == 32, "block scan assumes one (round, warp) entry per lane");
 static_assert(kTile == kDecThreads * 16, "decode sweep assumes 16 counts per thread");
 
@@ -30,30 +31,36 @@ enum : unsigned long long {
 struct alignas(256) Ctrl {
     long long k;                  // words of the last encode
     unsigned long long flags;     // sticky flags
-    unsigned int ticket[2];       // dynamic tile tickets, indexed by epoch parity
-    unsigned int epoch;           // look-back epoch of the NEXT encode, 1..kEpochMax
 };
 
-// Look-back tile descriptor: [epoch:30 | status:2 | value:32].  The epoch
-// lives on the device (Ctrl::epoch) and is advanced by the last tile, so an
-// encode needs no host state and can be captured in a CUDA graph.  Every call
-// rewrites every tile's descriptor, so a descriptor is never older than one
-// call and the epoch may wrap (kEpochMax -> 1) without a reset.
-enum : unsigned { kDescAggregate = 1u, kDescPrefix = 2u };
-constexpr unsigned kEpochMax = (1u << 30) - 1u;
-
+// Encode runs as two kernels (encode.cu):
+//   1. gtc_encode_tiles_kernel: CTA b streams a contiguous chunk of
+//      chunk_tiles tiles of g and r, writes r, compacts each tile's words into
+//      its slot of a tile-major scratch, writes the tile's word count and, at
+//      the end, its chunk's word count (every entry rewritten every call: no
+//      atomics, no zeroing, no state carried between calls);
+//   2. gtc_compact_kernel: one warp per tile turns the counts into global tile
+//      offsets (sum of earlier chunks + earlier tiles of its chunk) and copies
+//      the words into the contiguous message.
 struct EncodeParams {
     const float* g;          // may be null (residual already holds r + g)
     float* r;
     long long n;
     float tau;
-    unsigned int* words;     // message out
+    unsigned int* words;     // message out (contiguous)
     long long capacity;      // words available
-    unsigned long long* desc;  // [num_tiles] look-back descriptors
+    unsigned int* scratch;   // [num_tiles * kTile] tile-major words
+    int* tile_cnt;           // [num_tiles] words per tile
+    unsigned int* chunk_sum; // [num_chunks] words per chunk of kernel 1
     int* tile_off;           // [num_tiles + 1] exclusive word offsets per tile
     Ctrl* ctrl;
     int num_tiles;
+    int chunk_tiles;         // tiles per kernel-1 CTA (set by launch_encode)
+    int num_chunks;          // kernel-1 grid (set by launch_encode)
 };
+
+// Most kernel-1 CTAs (chunks) a launch may use: 148 SMs x 2, with headroom.
+constexpr int kMaxChunks = 1024;
 
 struct MsgSet {
     const unsigned int* words[GTC_MAX_MSGS];
@@ -70,6 +77,7 @@ struct DecodeParams {
     float* target;
     signed char* counts_out;   // may be null
     const unsigned long long* flags;  // skip everything if capacity/corrupt set
+    int tiles_per_cta;         // set by launch_decode_apply
 };
 
 struct BoundsParams {

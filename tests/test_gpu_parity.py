@@ -105,7 +105,8 @@ def test_config1_correlated_2workers_10steps(cmp):
 @pytest.mark.parametrize("cmp", ["gt", "ge"])
 @pytest.mark.parametrize("n", [1, 3, 4, 5, 31, 4095, 4096, 4097, 3 * 4096 + 1234, 65536 * 3 + 7])
 def test_single_rank_path_sizes(n, cmp):
-    """encode -> exchange (no-op) -> decode_apply at world=1, ragged sizes."""
+    """encode -> exchange (no-op) -> decode_apply at world=1, ragged sizes
+    (counts_out given: the tiled shared-memory count kernel)."""
     tau = 2.0
     g = synth.normal(n, 3, n) * np.float32(3.0)
     r_host = synth.uniform(n, -tau, tau, 4, n)
@@ -126,6 +127,47 @@ def test_single_rank_path_sizes(n, cmp):
     assert np.array_equal(cnt.cpu().numpy().astype(np.int32), oc)
     assert_float_parity(wd.cpu().numpy(), w_host, "weights")
     assert ctx.check() == gtc.GTC_OK
+    ctx.close()
+
+
+@pytest.mark.parametrize("mode", [gtc.GTC_ACCUM_WEIGHTS, gtc.GTC_ACCUM_UPDATE])
+@pytest.mark.parametrize("n", [1, 4097, 3 * 4096 + 1234, 2_000_003])
+@pytest.mark.parametrize("use_step", [False, True])
+def test_single_rank_word_parallel_apply(n, mode, use_step):
+    """world=1 without counts_out: the word-parallel apply kernel (and gtc_step)."""
+    tau = 0.1  # fl(c * tau) is inexact for general c, exact for c = +-1
+    g = synth.normal(n, 21, n) * np.float32(0.3)
+    r_host = synth.uniform(n, -tau, tau, 22, n)
+    w_host = synth.normal(n, 23, n)
+    ctx = gtc.GTC(n, tau)
+    rd, gd, wd = to_dev(r_host), to_dev(g), to_dev(w_host)
+    for t in range(3):
+        if use_step:
+            ctx.step(gd, rd, wd, -0.75, mode)
+        else:
+            ctx.encode(gd, rd)
+            ctx.exchange()
+            ctx.decode_apply(wd, -0.75, mode)
+        oracle.step([g], [r_host], w_host, tau, oracle.CMP_GT, -0.75, mode)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(rd), r_host.view(np.uint32))
+    assert_float_parity(wd.cpu().numpy(), w_host, "weights")
+    ctx.close()
+
+
+def test_sim_single_message_word_parallel():
+    """decode_apply_msgs with one message and no counts_out."""
+    n, tau = 300_007, 8.0
+    v = synth.normal(n, 24) * np.float32(9.0)
+    ctx = gtc.GTC(n, tau, max_sim_msgs=1)
+    rd = to_dev(v)
+    ctx.encode(None, rd)
+    wd = torch.zeros(n, device=DEV)
+    ctx.decode_apply_msgs([ctx.message()], wd, 2.0, gtc.GTC_ACCUM_WEIGHTS)
+    words, _ = oracle.encode(None, v.copy(), tau)
+    w_exp = np.zeros(n, np.float32)
+    oracle.apply(oracle.decode_counts([words], n), w_exp, tau, 2.0, oracle.ACCUM_WEIGHTS)
+    assert_float_parity(wd.cpu().numpy(), w_exp, "weights")
     ctx.close()
 
 

@@ -1,0 +1,105 @@
+"""Diagnose step time: device time with/without per-kernel events, host issue
+time per step, and CUDA-graph replay of the same steps (world = 1)."""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1904_10584_b200 as gtc  # noqa: E402
+import synth  # noqa: E402
+
+
+def main():
+    n, tau, rho = synth.LSTM_AM_PARAMS, 8.0, 0.01
+    dev = torch.device("cuda", 0)
+    sigma = synth.sigma_for_density(rho, tau, synth.mean_abs_scale(n))
+    grads = [torch.from_numpy(synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, 0)).to(dev) for t in range(3)]
+    r = torch.from_numpy(synth.uniform(n, -tau, tau, 1)).to(dev)
+    w = torch.zeros(n, device=dev)
+    ctx = gtc.GTC(n, tau)
+    s = torch.cuda.current_stream()
+
+    def step(t):
+        ctx.encode(grads[t % 3], r)
+        ctx.exchange()
+        ctx.decode_apply(w, -1e-3)
+
+    for t in range(50):
+        step(t)
+    torch.cuda.synchronize()
+    K = 2000
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    c0 = time.perf_counter()
+    for t in range(K):
+        step(t)
+    c1 = time.perf_counter()
+    e1.record(s)
+    torch.cuda.synchronize()
+    print(f"plain loop: device {e0.elapsed_time(e1) / K * 1e3:.1f} us/step, host issue {(c1 - c0) / K * 1e6:.1f} us/step")
+
+    f = ctx.stepper(grads, r, w, -1e-3)
+    torch.cuda.synchronize()
+    e0.record(s)
+    c0 = time.perf_counter()
+    for t in range(K):
+        f(t)
+    c1 = time.perf_counter()
+    e1.record(s)
+    torch.cuda.synchronize()
+    print(f"stepper loop: device {e0.elapsed_time(e1) / K * 1e3:.1f} us/step, host issue {(c1 - c0) / K * 1e6:.1f} us/step")
+
+    # encode only / decode only
+    for name, fn in [("encode only", lambda t: ctx.encode(grads[t % 3], r)),
+                     ("decode only", lambda t: (ctx.exchange(), ctx.decode_apply(w, -1e-3)))]:
+        if name == "decode only":
+            ctx.encode(grads[0], r)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for t in range(K):
+            if name == "decode only":
+                ctx.exchange()
+                ctx.decode_apply(w, -1e-3)
+                ctx.encode(None, r) if False else None
+                # decode needs an encode between calls (state machine): re-encode with g=None is extra work;
+                # instead time decode via events around a single call
+            else:
+                fn(t)
+            if name == "decode only":
+                break
+        e1.record(s)
+        torch.cuda.synchronize()
+        if name == "encode only":
+            print(f"{name}: {e0.elapsed_time(e1) / K * 1e3:.1f} us/launch pair")
+
+    # CUDA graph of G steps
+    G = 20
+    gs = torch.cuda.Stream()
+    gs.wait_stream(s)
+    with torch.cuda.stream(gs):
+        for t in range(3):
+            step(t)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=gs):
+        for t in range(G):
+            ctx.encode(grads[t % 3], r, stream=gs)
+            ctx.exchange(stream=gs)
+            ctx.decode_apply(w, -1e-3, stream=gs)
+    for _ in range(5):
+        graph.replay()
+    torch.cuda.synchronize()
+    R = 100
+    e0.record(s)
+    for _ in range(R):
+        graph.replay()
+    e1.record(s)
+    torch.cuda.synchronize()
+    print(f"cuda graph: device {e0.elapsed_time(e1) / (R * G) * 1e3:.1f} us/step")
+
+
+if __name__ == "__main__":
+    main()
