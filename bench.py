@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--tau", type=float, default=8.0, help="gradient threshold (PAPER.md:249 uses 8)")
     ap.add_argument("--cmp", choices=["gt", "ge"], default="gt")
     ap.add_argument("--alpha", type=float, default=-1e-3, help="apply scale (e.g. -lr)")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="world > 1: NVLink peer reads fused into decode (p2p) or NCCL all-gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -229,7 +231,7 @@ def run_gtc(args):
     grads = [torch.from_numpy(g).to(dev) for g in grads_h]
     r = torch.from_numpy(r0_h).to(dev)
     w = torch.from_numpy(w0_h).to(dev)
-    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp)
+    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp, exchange=args.exchange)
     stream = torch.cuda.current_stream(dev)
 
     def step(t):
@@ -376,6 +378,7 @@ def run_gtc(args):
         "config": {"workload": args.workload, "desc": wl["desc"], "n_params": n, "tau": tau,
                    "rho_target": args.rho, "rho_measured": k_rank / n, "cmp": args.cmp,
                    "parallelism": f"dp{world}", "apply": "ACCUM_WEIGHTS",
+                   "exchange": ctx.exchange_mode(),
                    "l2": f"inputs larger than L2: g rotates over {N_GRAD_BUFFERS} buffers, "
                          f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": "gtc_encode_kernel", "achieved": enc_gbs, "peak": peak,

@@ -76,12 +76,21 @@ typedef enum {
     GTC_ECORRUPT = 7,    /* a message word is out of range or not ascending      */
     GTC_ESTATE = 8,      /* call out of order / workspace not bound              */
     GTC_ECAPACITY = 9,   /* a message exceeded max_words_per_rank                 */
-    GTC_EUNSUPPORTED = 10 /* e.g. world > GTC_MAX_MSGS                           */
+    GTC_EUNSUPPORTED = 10,/* e.g. world > GTC_MAX_MSGS, p2p mapping impossible   */
+    GTC_EPEER = 11       /* p2p: a peer did not publish its message within 30 s
+                            (nothing was applied)                                 */
 } gtc_status;
 
 /* Threshold comparison (R1). */
 enum { GTC_CMP_GT = 0, /* paper, "greater than": |v| > tau (default) */
        GTC_CMP_GE = 1  /* BASELINE.json north_star: |v| >= tau             */ };
+
+/* Exchange mode for world > 1 (OR-ed into gtc_init's flags). */
+enum { GTC_EXCHANGE_P2P = 0,     /* default: peers' messages are read straight from
+                                    their memory over NVLink (CUDA IPC mapping made at
+                                    bind time); no host sync, no staging copy     */
+       GTC_EXCHANGE_NCCL = 16    /* ncclAllGather of counts, one host wait, then
+                                    ncclAllGather of the words and tile offsets  */ };
 
 /* What decode_apply updates (R8). */
 enum { GTC_ACCUM_WEIGHTS = 0, /* target[i] = fmaf(alpha, fl(c[i]*tau), target[i]) */
@@ -103,7 +112,8 @@ gtc_status gtc_get_unique_id(void* out_128_bytes);
  *  rank/world : this process's rank, number of data-parallel workers.
  *  nccl_unique_id : 128 bytes from gtc_get_unique_id on rank 0; NULL iff world == 1.
  *  cuda_device: device ordinal this rank runs on (made current for the call).
- *  flags      : GTC_CMP_GT or GTC_CMP_GE.
+ *  flags      : GTC_CMP_GT or GTC_CMP_GE, OR-ed with GTC_EXCHANGE_P2P (default) or
+ *               GTC_EXCHANGE_NCCL.
  * On success *out is a new context (free with gtc_destroy). Blocks on NCCL
  * communicator creation when world > 1. */
 gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int world,
@@ -118,7 +128,11 @@ gtc_status gtc_workspace_size(const gtc_ctx* ctx, int64_t max_words_per_rank,
 /* Hand the workspace to the context (256-byte aligned, >= the size above for
  * the SAME max_words_per_rank / max_sim_msgs).  Initialises it with a
  * synchronous cudaMemset.  The caller keeps ownership and must keep it alive
- * until gtc_destroy. */
+ * until gtc_destroy.  world > 1, p2p mode: collective over all ranks (every
+ * rank binds with the same sizes); exports this workspace with CUDA IPC and
+ * maps every peer's (GTC_EUNSUPPORTED if that is impossible on any rank: use
+ * GTC_EXCHANGE_NCCL).  The workspace must come from cudaMalloc (e.g. PyTorch's
+ * default caching allocator), not from a virtual-memory-mapped pool. */
 gtc_status gtc_bind_workspace(gtc_ctx* ctx, void* dev_ptr, size_t bytes,
                               int64_t max_words_per_rank, int max_sim_msgs);
 
@@ -131,15 +145,22 @@ gtc_status gtc_bind_workspace(gtc_ctx* ctx, void* dev_ptr, size_t bytes,
  * offsets stay in the workspace (see gtc_message / gtc_local_count). */
 gtc_status gtc_encode(gtc_ctx* ctx, const float* grad, float* residual, cudaStream_t stream);
 
-/* All-gather of every rank's message (world > 1): ncclAllGather of (k, flags),
- * ONE host wait for the counts, then ncclAllGather of the words padded to the
- * largest k and of the per-tile offsets.  world == 1: no device work.
- * Returns GTC_ENONFINITE if any rank flagged a non-finite residual (the
- * exchange still completed; decode_apply may proceed), GTC_ECAPACITY if any
- * rank's k exceeded the capacity (nothing exchanged). */
+/* Make every rank's message available to every other rank (world > 1).
+ *  p2p : one single-warp kernel publishes "step e ready" into every peer's
+ *        ready flags over NVLink (release, system scope); no host wait.
+ *        Errors of any rank are reported by gtc_check after decode_apply.
+ *  nccl: ncclAllGather of (k, flags), ONE host wait for the counts, then
+ *        ncclAllGather of the words padded to the largest k and of the
+ *        per-tile offsets.  Returns GTC_ENONFINITE if any rank flagged a
+ *        non-finite residual (the exchange still completed; decode_apply may
+ *        proceed), GTC_ECAPACITY if any rank's k exceeded the capacity.
+ * world == 1: no device work. */
 gtc_status gtc_exchange(gtc_ctx* ctx, cudaStream_t stream);
 
-/* Steps 5-6 of P:222 on `stream`: signed integer counts of all ranks' quanta
+/* Steps 5-6 of P:222 on `stream` (p2p: the kernel first waits, on the device,
+ * for every peer's ready flag of this step, then reads the peers' messages
+ * over NVLink; if any rank overflowed its capacity or a peer timed out,
+ * nothing is applied and gtc_check reports it): signed integer counts of all ranks' quanta
  * (deterministic, atomic-free, rank order irrelevant) and the apply of
  * count * tau to target (float[n] device, in/out) for every element with a
  * non-zero count (mode GTC_ACCUM_WEIGHTS with alpha, or GTC_ACCUM_UPDATE).
@@ -177,9 +198,17 @@ gtc_status gtc_local_count(const gtc_ctx* ctx, const int64_t** dev_k);
  * (world == 1: the local message; k is read back, waiting on the stream). */
 gtc_status gtc_message(gtc_ctx* ctx, int rank, const uint32_t** dev_words, int64_t* k);
 
+/* Copy rank `rank`'s message of the last step into host memory (tests,
+ * debugging; waits for the device).  max_words is the room at host_words. */
+gtc_status gtc_read_message(gtc_ctx* ctx, int rank, uint32_t* host_words, int64_t max_words, int64_t* k);
+
 /* Wait for `stream`, then report and clear the sticky device flags:
- * GTC_ENONFINITE, GTC_ECAPACITY, GTC_ECORRUPT or GTC_OK. */
+ * GTC_EPEER, GTC_ECAPACITY, GTC_ECORRUPT, GTC_ENONFINITE or GTC_OK (p2p: the
+ * flags of every rank of the last decode_apply are folded in). */
 gtc_status gtc_check(gtc_ctx* ctx, cudaStream_t stream);
+
+/* GTC_EXCHANGE_P2P or GTC_EXCHANGE_NCCL (world > 1), 0 for world == 1. */
+int gtc_exchange_mode(const gtc_ctx* ctx);
 
 /* Number of kernels libgtc launched on this context so far (NCCL's excluded). */
 int64_t gtc_kernel_launches(const gtc_ctx* ctx);

@@ -31,9 +31,12 @@ GTC_ECORRUPT = 7
 GTC_ESTATE = 8
 GTC_ECAPACITY = 9
 GTC_EUNSUPPORTED = 10
+GTC_EPEER = 11
 
 GTC_CMP_GT = 0
 GTC_CMP_GE = 1
+GTC_EXCHANGE_P2P = 0
+GTC_EXCHANGE_NCCL = 16
 GTC_ACCUM_WEIGHTS = 0
 GTC_ACCUM_UPDATE = 1
 GTC_MAX_MSGS = 64
@@ -55,7 +58,9 @@ _SIGS = {
     "gtc_last_counts": (_i32, [_vp, _vp]),
     "gtc_local_count": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "gtc_message": (_i32, [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]),
+    "gtc_read_message": (_i32, [_vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]),
     "gtc_check": (_i32, [_vp, _vp]),
+    "gtc_exchange_mode": (_i32, [_vp]),
     "gtc_kernel_launches": (_i64, [_vp]),
     "gtc_strerror": (ctypes.c_char_p, [_i32]),
     "gtc_last_error_detail": (ctypes.c_char_p, [_vp]),
@@ -170,6 +175,21 @@ def gtc_message(ctx, rank: int):
     return p.value, k.value
 
 
+def gtc_read_message(ctx, rank: int, max_words: int):
+    """Host copy (numpy uint32) of a rank's message of the last step."""
+    import numpy as np
+
+    buf = np.empty(max(max_words, 1), dtype=np.uint32)
+    k = _i64()
+    _chk(load_library().gtc_read_message(ctx, rank, buf.ctypes.data_as(_vp), max_words, ctypes.byref(k)),
+         "gtc_read_message", ctx)
+    return buf[: k.value].copy()
+
+
+def gtc_exchange_mode(ctx) -> int:
+    return load_library().gtc_exchange_mode(ctx)
+
+
 def gtc_check(ctx, stream: int) -> int:
     return load_library().gtc_check(ctx, stream)
 
@@ -231,7 +251,8 @@ class GTC:
     """
 
     def __init__(self, n_params: int, tau: float, rank: int = 0, world: int = 1, device=None,
-                 cmp: str = "gt", max_words_per_rank: int = 0, max_sim_msgs: int = 0, group=None):
+                 cmp: str = "gt", max_words_per_rank: int = 0, max_sim_msgs: int = 0, group=None,
+                 exchange: str = "p2p"):
         import torch
 
         if not torch.cuda.is_available():
@@ -239,11 +260,13 @@ class GTC:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.n, self.tau, self.rank, self.world = int(n_params), float(tau), int(rank), int(world)
         self.cmp = {"gt": GTC_CMP_GT, "ge": GTC_CMP_GE}[cmp]
+        flags = self.cmp | {"p2p": GTC_EXCHANGE_P2P, "nccl": GTC_EXCHANGE_NCCL}[exchange]
+        self.max_words = max_words_per_rank if max_words_per_rank > 0 else self.n
         uid = None
         if world > 1:
             uid = broadcast_unique_id(rank, group)
         with torch.cuda.device(self.device):
-            self.ctx = gtc_init(self.n, self.tau, rank, world, uid, self.device.index, self.cmp)
+            self.ctx = gtc_init(self.n, self.tau, rank, world, uid, self.device.index, flags)
             nbytes = gtc_workspace_size(self.ctx, max_words_per_rank, max_sim_msgs)
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             gtc_bind_workspace(self.ctx, self.workspace.data_ptr(), nbytes, max_words_per_rank, max_sim_msgs)
@@ -319,11 +342,24 @@ class GTC:
         """(device pointer, k) of a rank's message (local one when world == 1)."""
         return gtc_message(self.ctx, self.rank if rank is None else rank)
 
+    def read_message(self, rank: int | None = None):
+        """Host (numpy uint32) copy of a rank's message of the last step (any world)."""
+        return gtc_read_message(self.ctx, self.rank if rank is None else rank, self.max_words)
+
+    def exchange_mode(self) -> str:
+        m = gtc_exchange_mode(self.ctx)
+        return {0: "local", GTC_EXCHANGE_P2P: "p2p", GTC_EXCHANGE_NCCL: "nccl"}.get(m, "?") if self.world > 1 \
+            else "local"
+
     def message_tensor(self, rank: int | None = None):
-        """The message as an int32 view into the workspace (bit pattern = uint32 words)."""
+        """The message as an int32 view into this rank's workspace (bit pattern =
+        uint32 words).  Only for messages that live in this workspace (world 1,
+        or NCCL mode); use read_message() for peers' messages in p2p mode."""
         import torch
 
         ptr, k = self.message(rank)
+        if not (self.workspace.data_ptr() <= ptr < self.workspace.data_ptr() + self.workspace.numel()):
+            raise ValueError("message is not in this rank's workspace; use read_message()")
         off = ptr - self.workspace.data_ptr()
         return self.workspace[off: off + 4 * k].view(torch.int32)
 

@@ -34,14 +34,69 @@ constexpr int kPreMsgs = 8;             // messages whose first words are preloa
 constexpr int kMaxTouched = 4096;       // non-zero counts applied through the list
 constexpr int kChunksPerThread = kDecMaxTilesPerCta * (kTile / 16) / kDecThreads;
 
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr unsigned long long kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000;
+
+// p2p exchange gate (thread 0 of every CTA): wait until every peer has
+// published this step's message (ready[r] >= epoch: a peer can be at most one
+// step ahead, because its next decode waits for this rank's next signal),
+// then fold every rank's header flags.  Returns the flags; a capacity
+// overflow anywhere or a timed-out peer means nothing is applied anywhere.
+__device__ unsigned long long p2p_gate(const DecodeParams& p) {
+    unsigned long long f = 0;
+    const unsigned long long t0 = globaltimer_ns();
+    for (int r = 0; r < p.nmsg; ++r) {
+        if (r == p.self) continue;
+        while (ld_acquire_sys(&p.ready[r]) < p.epoch) {
+            if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+                f |= kFlagPeer;
+                break;
+            }
+            __nanosleep(64);
+        }
+        if (f & kFlagPeer) break;
+    }
+    if (!(f & kFlagPeer))
+        for (int r = 0; r < p.nmsg; ++r) f |= ld_relaxed_sys(&p.hdr[r]->flags);
+    return f;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const DecodeParams p) {
     extern __shared__ int4 s_cnt4[];  // tiles_per_cta * kTile int8 counts
     __shared__ int s_rng[GTC_MAX_MSGS][2];
     __shared__ unsigned s_warp[kDecThreads / 32];
     __shared__ unsigned short s_list[kMaxTouched];  // local indices with c != 0 (< 32768)
+    __shared__ unsigned long long s_gate;
 
     if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;  // nothing is applied
+    if (p.ready) {
+        if (threadIdx.x == 0) {
+            const unsigned long long f = p2p_gate(p);
+            s_gate = f;
+            if (blockIdx.x == 0 && (f & (kFlagNonFinite | kFlagCapacity | kFlagPeer)))
+                atomicOr(p.local_flags, f & (kFlagNonFinite | kFlagCapacity | kFlagPeer));
+        }
+        __syncthreads();
+        if (s_gate & (kFlagCapacity | kFlagPeer)) return;
+    }
 
     signed char* s_cnt = reinterpret_cast<signed char*>(s_cnt4);
     const int tid = threadIdx.x;
@@ -302,6 +357,24 @@ cudaError_t launch_decode_apply(const DecodeParams& p_in, int accum_mode, cudaSt
         gtc_decode_apply_kernel<GTC_ACCUM_UPDATE><<<grid, kDecThreads, smem, s>>>(p);
     else
         gtc_decode_apply_kernel<GTC_ACCUM_WEIGHTS><<<grid, kDecThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+// p2p exchange: publish "this rank's message of step `epoch` is ready" into
+// every peer's ready[self] (remote store over NVLink, release at system scope
+// after a system fence; the message itself was written by the preceding
+// encode kernels on the same stream).
+__global__ void gtc_signal_kernel(const SignalParams p) {
+    const int r = threadIdx.x;
+    if (r < p.world && r != p.self) {
+        __threadfence_system();
+        unsigned long long* a = p.peer_ready[r] + p.self;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(a), "l"(p.epoch) : "memory");
+    }
+}
+
+cudaError_t launch_signal(const SignalParams& p, cudaStream_t s) {
+    gtc_signal_kernel<<<1, 64, 0, s>>>(p);
     return cudaGetLastError();
 }
 

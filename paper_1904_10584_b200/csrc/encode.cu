@@ -304,7 +304,13 @@ __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const Enco
             const long long k = dst0 + my_cnt;
             p.tile_off[p.num_tiles] = (int)k;
             p.ctrl->k = k;
-            if (k > p.capacity) atomicOr(&p.ctrl->flags, kFlagCapacity);
+            unsigned long long f = *reinterpret_cast<volatile unsigned long long*>(&p.ctrl->flags);
+            if (k > p.capacity) {
+                atomicOr(&p.ctrl->flags, kFlagCapacity);
+                f |= kFlagCapacity;
+            }
+            p.hdr->k = k;
+            p.hdr->flags = f;
         }
     }
     const unsigned* src = p.scratch + (long long)tile * kTile;

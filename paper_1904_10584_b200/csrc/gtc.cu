@@ -1,7 +1,17 @@
 // gtc.cu -- the C ABI of libgtc.so (include/gtc.h): context, workspace layout,
-// argument validation, call ordering and the NCCL exchange (PAPER.md:222
-// "Each worker communicates the sparse update to all other workers and
-// conversely receives all sparse updates from other workers").
+// argument validation, call ordering and the exchange ("Each
+// worker communicates the sparse update to all other workers and conversely
+// receives all sparse updates from other workers").
+//
+// Two exchange modes for world > 1:
+//   p2p  (default): every rank's workspace is mapped into its peers with CUDA
+//        IPC at bind time.  gtc_exchange launches a one-warp signal kernel that
+//        publishes "message of step e ready" into every peer's ready[] array
+//        over NVLink; gtc_decode_apply reads every rank's header, tile offsets
+//        and words straight from the owner's memory over NVLink.  No host sync,
+//        no staging copy; messages are double-buffered by step parity.
+//   nccl (GTC_EXCHANGE_NCCL): ncclAllGather of (k, flags), one host wait for
+//        the largest k, then ncclAllGather of the words and tile offsets.
 #include <nccl.h>
 
 #include <algorithm>
@@ -22,42 +32,78 @@ enum class Stage { kBound, kEncoded, kExchanged };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// A message region: header | tile offsets | words.  Same layout on every rank.
+struct Region {
+    size_t hdr, tile_off, words, bytes;
+};
+
+Region make_region(long long tiles, long long capacity) {
+    Region R{};
+    size_t o = 0;
+    R.hdr = o;      o = align_up(o + sizeof(MsgHeader), 256);
+    R.tile_off = o; o = align_up(o + sizeof(int) * (size_t)(tiles + 1), 256);
+    R.words = o;    o = align_up(o + sizeof(unsigned) * (size_t)std::max(capacity, 1LL), 256);
+    R.bytes = o;
+    return R;
+}
+
 // Workspace layout (offsets from the bound base, each 256-byte aligned):
 //   ctrl      Ctrl                              k, flags
 //   chunk_sum u32[kMaxChunks]                   words per encode-kernel-1 chunk
 //   tile_cnt  i32[num_tiles]                    words per tile
-//   tile_off  i32[num_tiles + 1]                this rank's tile offsets
 //   scratch   u32[num_tiles * kTile]            tile-major words (encode kernel 1)
-//   send      u32[capacity]                     this rank's message
-//   kx_all    i64[2 * world]                    all-gathered (k, flags)   (world > 1)
-//   recv      u32[world * capacity]             all-gathered messages     (world > 1)
-//   recv_off  i32[world * (num_tiles + 1)]      all-gathered tile offsets (world > 1)
+//   region    Region x (1, or 2 for p2p)        header | tile offsets | words
+//   ready     u64[world]                        p2p: written by peers over NVLink
+//   ipc       128 B x world                     p2p: bind-time handle exchange
+//   kx_all    i64[2 * world]                    nccl: all-gathered (k, flags)
+//   recv      u32[world * capacity]             nccl: all-gathered messages
+//   recv_off  i32[world * (num_tiles + 1)]      nccl: all-gathered tile offsets
 //   sim_off   i32[max_sim_msgs * (num_tiles+1)] tile offsets for decode_apply_msgs
 struct Layout {
-    size_t ctrl, chunk_sum, tile_cnt, tile_off, scratch, send, kx_all, recv, recv_off, sim_off, total;
+    Region R;
+    int nregions;
+    size_t ctrl, chunk_sum, tile_cnt, scratch, region[2], ready, ipc, kx_all, recv, recv_off, sim_off, total;
 };
 
-Layout make_layout(long long n, int world, long long capacity, int max_sim_msgs) {
+constexpr size_t kIpcRecord = 128;
+
+Layout make_layout(long long n, int world, bool p2p, long long capacity, int max_sim_msgs) {
     const long long tiles = (n + kTile - 1) / kTile;
     Layout L{};
     size_t o = 0;
     L.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
     L.chunk_sum = o; o = align_up(o + sizeof(unsigned) * (size_t)kMaxChunks, 256);
     L.tile_cnt = o;  o = align_up(o + sizeof(int) * (size_t)std::max(tiles, 1LL), 256);
-    L.tile_off = o;  o = align_up(o + sizeof(int) * (size_t)(tiles + 1), 256);
     L.scratch = o;   o = align_up(o + sizeof(unsigned) * (size_t)std::max(tiles, 1LL) * kTile, 256);
-    L.send = o;      o = align_up(o + sizeof(unsigned) * (size_t)std::max(capacity, 1LL), 256);
-    if (world > 1) {
+    L.R = make_region(tiles, capacity);
+    L.nregions = (world > 1 && p2p) ? 2 : 1;
+    for (int i = 0; i < 2; ++i) {
+        L.region[i] = o;
+        if (i < L.nregions) o += L.R.bytes;
+    }
+    L.ready = L.ipc = L.kx_all = L.recv = L.recv_off = 0;
+    if (world > 1 && p2p) {
+        L.ready = o; o = align_up(o + sizeof(unsigned long long) * (size_t)world, 256);
+        L.ipc = o;   o = align_up(o + kIpcRecord * (size_t)world, 256);
+    } else if (world > 1) {
+        L.ipc = o;      o = align_up(o + kIpcRecord * (size_t)world, 256);
         L.kx_all = o;   o = align_up(o + sizeof(long long) * 2 * (size_t)world, 256);
         L.recv = o;     o = align_up(o + sizeof(unsigned) * (size_t)world * (size_t)std::max(capacity, 1LL), 256);
         L.recv_off = o; o = align_up(o + sizeof(int) * (size_t)world * (size_t)(tiles + 1), 256);
-    } else {
-        L.kx_all = L.recv = L.recv_off = 0;
     }
     L.sim_off = o;   o = align_up(o + sizeof(int) * (size_t)std::max(max_sim_msgs, 0) * (size_t)(tiles + 1), 256);
     L.total = o;
     return L;
 }
+
+struct IpcRecord {
+    cudaIpcMemHandle_t handle;   // 64 B, of the allocation holding the workspace
+    unsigned long long offset;   // workspace base - allocation base
+    unsigned long long total;    // layout size (must agree on every rank)
+    int ok;                      // this rank could export its workspace
+    int device;
+};
+static_assert(sizeof(IpcRecord) <= kIpcRecord, "IPC record fits its slot");
 
 }  // namespace
 
@@ -66,6 +112,7 @@ struct gtc_ctx {
     float tau = 0.f;
     int rank = 0, world = 1, device = 0;
     int cmp_mode = GTC_CMP_GT;
+    bool p2p = false;
     int num_tiles = 0;
     ncclComm_t comm = nullptr;
 
@@ -78,13 +125,16 @@ struct gtc_ctx {
     Ctrl* ctrl = nullptr;
     unsigned* chunk_sum = nullptr;
     int* tile_cnt = nullptr;
-    int* tile_off = nullptr;
     unsigned* scratch = nullptr;
-    unsigned* send = nullptr;
     long long* kx_all = nullptr;
     unsigned* recv = nullptr;
     int* recv_off = nullptr;
     int* sim_off = nullptr;
+
+    // p2p: every rank's workspace base as seen from this process (self = ws)
+    std::vector<unsigned char*> peer_ws;
+    std::vector<void*> peer_alloc;  // what cudaIpcOpenMemHandle returned (to close)
+    unsigned long long epoch = 0;   // p2p step counter; parity selects the region
 
     long long* host_kx = nullptr;  // pinned, 2 * world
     std::vector<long long> last_k;
@@ -126,9 +176,102 @@ struct DeviceGuard {
 };
 
 gtc_status flags_to_status(unsigned long long f) {
+    if (f & kFlagPeer) return GTC_EPEER;
     if (f & kFlagCapacity) return GTC_ECAPACITY;
     if (f & kFlagCorrupt) return GTC_ECORRUPT;
     if (f & kFlagNonFinite) return GTC_ENONFINITE;
+    return GTC_OK;
+}
+
+// The region (of this rank or a peer) a step's message lives in.
+unsigned char* region_base(const gtc_ctx* c, int rank, int parity) {
+    unsigned char* base = (c->world > 1 && c->p2p) ? c->peer_ws[rank] : c->ws;
+    return base + c->L.region[parity];
+}
+
+int cur_parity(const gtc_ctx* c) { return (c->world > 1 && c->p2p) ? (int)(c->epoch & 1ull) : 0; }
+
+// Base address of the allocation holding p (driver API, resolved at run time
+// so that libgtc.so does not link libcuda).
+typedef int (*MemGetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+bool allocation_base(const void* p, unsigned long long* base) {
+    static MemGetAddressRangeFn fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return false;
+        fn = reinterpret_cast<MemGetAddressRangeFn>(f);
+    }
+    size_t size = 0;
+    return fn(base, &size, reinterpret_cast<unsigned long long>(p)) == 0;
+}
+
+// p2p: export this rank's workspace, all-gather the records over NCCL, map
+// every peer's workspace.  All ranks agree on the outcome.
+gtc_status connect_peers(gtc_ctx* c) {
+    IpcRecord rec{};
+    unsigned long long base = 0;
+    rec.ok = allocation_base(c->ws, &base) && cudaIpcGetMemHandle(&rec.handle, reinterpret_cast<void*>(base)) == cudaSuccess;
+    cudaGetLastError();
+    rec.offset = rec.ok ? reinterpret_cast<unsigned long long>(c->ws) - base : 0ull;
+    rec.total = c->L.total;
+    rec.device = c->device;
+    unsigned char* slots = c->ws + c->L.ipc;
+    cudaError_t e = cudaMemcpy(slots + kIpcRecord * c->rank, &rec, sizeof(rec), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ipc record");
+    ncclResult_t r = ncclAllGather(slots + kIpcRecord * c->rank, slots, kIpcRecord, ncclUint8, c->comm, 0);
+    if (r != ncclSuccess) return nccl_fail(c, r, "bind: ncclAllGather(ipc)");
+    e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ipc sync");
+    std::vector<unsigned char> all(kIpcRecord * c->world);
+    e = cudaMemcpy(all.data(), slots, all.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ipc readback");
+    c->peer_ws.assign(c->world, nullptr);
+    c->peer_alloc.assign(c->world, nullptr);
+    int ok = 1;
+    for (int i = 0; i < c->world; ++i) {
+        IpcRecord ri;
+        std::memcpy(&ri, all.data() + kIpcRecord * i, sizeof(ri));
+        if (!ri.ok || ri.total != c->L.total) ok = 0;
+    }
+    if (ok) {
+        for (int i = 0; i < c->world; ++i) {
+            if (i == c->rank) {
+                c->peer_ws[i] = c->ws;
+                continue;
+            }
+            IpcRecord ri;
+            std::memcpy(&ri, all.data() + kIpcRecord * i, sizeof(ri));
+            void* p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, ri.handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                ok = 0;
+                break;
+            }
+            c->peer_alloc[i] = p;
+            c->peer_ws[i] = static_cast<unsigned char*>(p) + ri.offset;
+        }
+    }
+    // agree: every rank must have mapped every peer
+    int* okd = reinterpret_cast<int*>(slots);
+    e = cudaMemcpy(okd + c->rank, &ok, sizeof(int), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ok flag");
+    r = ncclAllGather(okd + c->rank, okd, 1, ncclInt32, c->comm, 0);
+    if (r != ncclSuccess) return nccl_fail(c, r, "bind: ncclAllGather(ok)");
+    std::vector<int> oks(c->world, 0);
+    e = cudaMemcpy(oks.data(), okd, sizeof(int) * c->world, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ok readback");
+    for (int v : oks) ok &= v;
+    if (!ok) {
+        for (void* p : c->peer_alloc)
+            if (p) cudaIpcCloseMemHandle(p);
+        c->peer_alloc.assign(c->world, nullptr);
+        return fail(c, GTC_EUNSUPPORTED,
+                    "p2p exchange: workspaces cannot be mapped across ranks (use GTC_EXCHANGE_NCCL)");
+    }
     return GTC_OK;
 }
 
@@ -149,6 +292,7 @@ const char* gtc_strerror(gtc_status s) {
         case GTC_ESTATE: return "call out of order or workspace not bound";
         case GTC_ECAPACITY: return "message exceeded max_words_per_rank";
         case GTC_EUNSUPPORTED: return "unsupported configuration";
+        case GTC_EPEER: return "a peer did not publish its message in time";
     }
     return "unknown status";
 }
@@ -172,7 +316,7 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     if (!(tau > 0.f) || std::isinf(tau)) return GTC_EINVAL;
     if (world < 1 || rank < 0 || rank >= world) return GTC_EINVAL;
     if (world > GTC_MAX_MSGS) return GTC_EUNSUPPORTED;
-    if (flags != GTC_CMP_GT && flags != GTC_CMP_GE) return GTC_EINVAL;
+    if (flags & ~(uint32_t)(GTC_CMP_GE | GTC_EXCHANGE_NCCL)) return GTC_EINVAL;
     if ((world > 1) != (nccl_unique_id != nullptr)) return GTC_EINVAL;
 
     gtc_ctx* c = new (std::nothrow) gtc_ctx();
@@ -182,7 +326,8 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     c->rank = rank;
     c->world = world;
     c->device = cuda_device;
-    c->cmp_mode = (int)flags;
+    c->cmp_mode = (int)(flags & GTC_CMP_GE);
+    c->p2p = world > 1 && !(flags & GTC_EXCHANGE_NCCL);
     c->num_tiles = (int)((n_params + kTile - 1) / kTile);
     c->last_k.assign(world, 0);
 
@@ -212,22 +357,27 @@ gtc_status gtc_workspace_size(const gtc_ctx* c, int64_t max_words_per_rank, int 
     if (!c || !bytes) return GTC_EINVAL;
     if (max_sim_msgs < 0 || max_sim_msgs > GTC_MAX_MSGS) return GTC_EINVAL;
     const long long cap = max_words_per_rank <= 0 ? c->n : std::min<long long>(max_words_per_rank, c->n);
-    *bytes = make_layout(c->n, c->world, cap, max_sim_msgs).total;
+    *bytes = make_layout(c->n, c->world, c->p2p, cap, max_sim_msgs).total;
     return GTC_OK;
 }
 
 gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t max_words_per_rank,
                               int max_sim_msgs) {
     if (!c || !dev_ptr) return fail(c, GTC_EINVAL, "bind: null");
+    if (c->bound) return fail(c, GTC_ESTATE, "bind: workspace already bound");
     if (reinterpret_cast<uintptr_t>(dev_ptr) & 255u) return fail(c, GTC_EALIGN, "workspace not 256-byte aligned");
     if (max_sim_msgs < 0 || max_sim_msgs > GTC_MAX_MSGS) return fail(c, GTC_EINVAL, "max_sim_msgs");
     const long long cap = max_words_per_rank <= 0 ? c->n : std::min<long long>(max_words_per_rank, c->n);
-    const Layout L = make_layout(c->n, c->world, cap, max_sim_msgs);
+    const Layout L = make_layout(c->n, c->world, c->p2p, cap, max_sim_msgs);
     if (bytes < L.total) return fail(c, GTC_EINVAL, "workspace too small");
     DeviceGuard g(c->device);
     unsigned char* b = static_cast<unsigned char*>(dev_ptr);
-    // Control block, chunk sums, counts and offsets start at 0.
+    // Control block, chunk sums and counts start at 0; so do the region
+    // headers/offsets and the p2p ready flags.
     cudaError_t e = cudaMemset(b, 0, L.scratch);
+    for (int i = 0; i < L.nregions && e == cudaSuccess; ++i)
+        e = cudaMemset(b + L.region[i], 0, L.R.words);
+    if (e == cudaSuccess && c->world > 1 && c->p2p) e = cudaMemset(b + L.ready, 0, L.ipc - L.ready);
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: cudaMemset");
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: sync");
@@ -239,15 +389,21 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     c->ctrl = reinterpret_cast<Ctrl*>(b + L.ctrl);
     c->chunk_sum = reinterpret_cast<unsigned*>(b + L.chunk_sum);
     c->tile_cnt = reinterpret_cast<int*>(b + L.tile_cnt);
-    c->tile_off = reinterpret_cast<int*>(b + L.tile_off);
     c->scratch = reinterpret_cast<unsigned*>(b + L.scratch);
-    c->send = reinterpret_cast<unsigned*>(b + L.send);
-    if (c->world > 1) {
+    if (c->world > 1 && !c->p2p) {
         c->kx_all = reinterpret_cast<long long*>(b + L.kx_all);
         c->recv = reinterpret_cast<unsigned*>(b + L.recv);
         c->recv_off = reinterpret_cast<int*>(b + L.recv_off);
     }
     c->sim_off = reinterpret_cast<int*>(b + L.sim_off);
+    if (c->world > 1 && c->p2p) {
+        gtc_status s = connect_peers(c);
+        if (s != GTC_OK) {
+            c->ws = nullptr;
+            return s;
+        }
+    }
+    c->epoch = 0;
     c->bound = true;
     c->stage = Stage::kBound;
     return GTC_OK;
@@ -260,9 +416,15 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     if (!aligned16(residual) || !aligned16(grad)) return fail(c, GTC_EALIGN, "encode: grad/residual alignment");
     DeviceGuard g(c->device);
 
+    c->epoch += 1;  // p2p: this step's epoch; its parity picks the message region
+    unsigned char* reg = region_base(c, c->rank, cur_parity(c));
+    MsgHeader* hdr = reinterpret_cast<MsgHeader*>(reg + c->L.R.hdr);
+    int* tile_off = reinterpret_cast<int*>(reg + c->L.R.tile_off);
+
     if (c->num_tiles == 0) {  // n == 0: empty message
         cudaError_t e = cudaMemsetAsync(&c->ctrl->k, 0, sizeof(long long), stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(c->tile_off, 0, sizeof(int), stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(hdr, 0, sizeof(MsgHeader), stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(tile_off, 0, sizeof(int), stream);
         if (e != cudaSuccess) return cuda_fail(c, e, "encode: n == 0");
         c->stage = Stage::kEncoded;
         return GTC_OK;
@@ -273,12 +435,13 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     p.r = residual;
     p.n = c->n;
     p.tau = c->tau;
-    p.words = c->send;
+    p.words = reinterpret_cast<unsigned*>(reg + c->L.R.words);
     p.capacity = c->capacity;
     p.scratch = c->scratch;
     p.tile_cnt = c->tile_cnt;
     p.chunk_sum = c->chunk_sum;
-    p.tile_off = c->tile_off;
+    p.tile_off = tile_off;
+    p.hdr = hdr;
     p.ctrl = c->ctrl;
     p.num_tiles = c->num_tiles;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
@@ -288,14 +451,7 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     return GTC_OK;
 }
 
-gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
-    if (!c) return GTC_EINVAL;
-    if (c->stage != Stage::kEncoded) return fail(c, GTC_ESTATE, "exchange: no encode since the last exchange");
-    if (c->world == 1) {
-        c->stage = Stage::kExchanged;
-        return GTC_OK;
-    }
-    DeviceGuard g(c->device);
+static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
     // 1. (k, flags) of every rank.  Ctrl::k and Ctrl::flags are adjacent.
     ncclResult_t r = ncclAllGather(&c->ctrl->k, c->kx_all, 2, ncclInt64, c->comm, stream);
     if (r != ncclSuccess) return nccl_fail(c, r, "exchange: ncclAllGather(counts)");
@@ -327,17 +483,42 @@ gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
     }
     c->max_k = max_k;
     // 3. words (padded to the largest k) and tile offsets, one NCCL group.
+    unsigned char* reg = c->ws + c->L.region[0];
     r = ncclGroupStart();
     if (r == ncclSuccess && max_k > 0)
-        r = ncclAllGather(c->send, c->recv, (size_t)max_k, ncclUint32, c->comm, stream);
+        r = ncclAllGather(reg + c->L.R.words, c->recv, (size_t)max_k, ncclUint32, c->comm, stream);
     if (r == ncclSuccess)
-        r = ncclAllGather(c->tile_off, c->recv_off, (size_t)c->num_tiles + 1, ncclInt32, c->comm, stream);
+        r = ncclAllGather(reg + c->L.R.tile_off, c->recv_off, (size_t)c->num_tiles + 1, ncclInt32, c->comm,
+                          stream);
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess) return nccl_fail(c, r, "exchange: ncclAllGather(words)");
     if (r2 != ncclSuccess) return nccl_fail(c, r2, "exchange: ncclGroupEnd");
     c->stage = Stage::kExchanged;
     return (any_flags & kFlagNonFinite) ? fail(c, GTC_ENONFINITE, "exchange: a rank saw a non-finite residual")
                                         : GTC_OK;
+}
+
+gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
+    if (!c) return GTC_EINVAL;
+    if (c->stage != Stage::kEncoded) return fail(c, GTC_ESTATE, "exchange: no encode since the last exchange");
+    if (c->world == 1) {
+        c->stage = Stage::kExchanged;
+        return GTC_OK;
+    }
+    DeviceGuard g(c->device);
+    if (!c->p2p) return exchange_nccl(c, stream);
+    // p2p: publish "step epoch ready" into every peer's ready[rank]
+    SignalParams sp{};
+    for (int i = 0; i < c->world; ++i)
+        sp.peer_ready[i] = reinterpret_cast<unsigned long long*>(c->peer_ws[i] + c->L.ready);
+    sp.world = c->world;
+    sp.self = c->rank;
+    sp.epoch = c->epoch;
+    cudaError_t e = launch_signal(sp, stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "exchange: signal launch");
+    c->launches += 1;
+    c->stage = Stage::kExchanged;
+    return GTC_OK;
 }
 
 static gtc_status check_apply_args(gtc_ctx* c, float* target, int mode) {
@@ -355,9 +536,20 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     if (s != GTC_OK) return s;
     DeviceGuard g(c->device);
     DecodeParams p{};
-    if (c->world == 1) {
-        p.m.words[0] = c->send;
-        p.m.off[0] = c->tile_off;
+    const int par = cur_parity(c);
+    if (c->world == 1 || c->p2p) {
+        for (int i = 0; i < c->world; ++i) {
+            unsigned char* reg = region_base(c, i, par);
+            p.m.words[i] = reinterpret_cast<const unsigned*>(reg + c->L.R.words);
+            p.m.off[i] = reinterpret_cast<const int*>(reg + c->L.R.tile_off);
+            p.hdr[i] = reinterpret_cast<const MsgHeader*>(reg + c->L.R.hdr);
+        }
+        if (c->world > 1) {
+            p.ready = reinterpret_cast<const unsigned long long*>(c->ws + c->L.ready);
+            p.epoch = c->epoch;
+            p.self = c->rank;
+            p.local_flags = &c->ctrl->flags;
+        }
     } else {
         for (int i = 0; i < c->world; ++i) {
             p.m.words[i] = c->recv + (size_t)i * (size_t)c->max_k;
@@ -458,15 +650,18 @@ gtc_status gtc_local_count(const gtc_ctx* c, const int64_t** dev_k) {
 gtc_status gtc_last_counts(gtc_ctx* c, int64_t* k_per_rank) {
     if (!c || !k_per_rank) return GTC_EINVAL;
     if (!c->bound) return fail(c, GTC_ESTATE, "last_counts: workspace not bound");
-    if (c->world == 1) {
-        DeviceGuard g(c->device);
-        long long k = 0;
-        cudaError_t e = cudaMemcpy(&k, &c->ctrl->k, sizeof(k), cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) return cuda_fail(c, e, "last_counts: readback");
-        k_per_rank[0] = k;
+    if (c->world > 1 && !c->p2p) {
+        for (int i = 0; i < c->world; ++i) k_per_rank[i] = c->last_k[i];
         return GTC_OK;
     }
-    for (int i = 0; i < c->world; ++i) k_per_rank[i] = c->last_k[i];
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    for (int i = 0; i < c->world && e == cudaSuccess; ++i) {
+        MsgHeader h{};
+        e = cudaMemcpy(&h, region_base(c, i, cur_parity(c)) + c->L.R.hdr, sizeof(h), cudaMemcpyDeviceToHost);
+        k_per_rank[i] = h.k;
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "last_counts: readback");
     return GTC_OK;
 }
 
@@ -474,16 +669,29 @@ gtc_status gtc_message(gtc_ctx* c, int rank, const uint32_t** dev_words, int64_t
     if (!c || !dev_words || !k) return GTC_EINVAL;
     if (!c->bound) return fail(c, GTC_ESTATE, "message: workspace not bound");
     if (rank < 0 || rank >= c->world) return fail(c, GTC_EINVAL, "message: rank");
-    if (c->world == 1) {
-        int64_t kk = 0;
-        gtc_status s = gtc_last_counts(c, &kk);
-        if (s != GTC_OK) return s;
-        *dev_words = c->send;
-        *k = kk;
+    if (c->world > 1 && !c->p2p) {
+        *dev_words = c->recv + (size_t)rank * (size_t)c->max_k;
+        *k = c->last_k[rank];
         return GTC_OK;
     }
-    *dev_words = c->recv + (size_t)rank * (size_t)c->max_k;
-    *k = c->last_k[rank];
+    std::vector<int64_t> ks(c->world);
+    gtc_status s = gtc_last_counts(c, ks.data());
+    if (s != GTC_OK) return s;
+    *dev_words = reinterpret_cast<const uint32_t*>(region_base(c, rank, cur_parity(c)) + c->L.R.words);
+    *k = ks[rank];
+    return GTC_OK;
+}
+
+gtc_status gtc_read_message(gtc_ctx* c, int rank, uint32_t* host_words, int64_t max_words, int64_t* k) {
+    if (!c || !k) return GTC_EINVAL;
+    const uint32_t* dev = nullptr;
+    gtc_status s = gtc_message(c, rank, &dev, k);
+    if (s != GTC_OK) return s;
+    if (*k > max_words || (*k > 0 && !host_words)) return fail(c, GTC_EINVAL, "read_message: buffer too small");
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && *k > 0) e = cudaMemcpy(host_words, dev, sizeof(uint32_t) * (size_t)*k, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "read_message: copy");
     return GTC_OK;
 }
 
@@ -504,11 +712,25 @@ gtc_status gtc_check(gtc_ctx* c, cudaStream_t stream) {
     return flags_to_status(f);
 }
 
+int gtc_exchange_mode(const gtc_ctx* c) {
+    if (!c) return -1;
+    return c->world == 1 ? 0 : (c->p2p ? GTC_EXCHANGE_P2P : GTC_EXCHANGE_NCCL);
+}
+
 int64_t gtc_kernel_launches(const gtc_ctx* c) { return c ? c->launches : 0; }
 
 void gtc_destroy(gtc_ctx* c) {
     if (!c) return;
     DeviceGuard g(c->device);
+    if (c->world > 1) cudaDeviceSynchronize();
+    if (c->bound && c->p2p && c->comm) {
+        // barrier: no peer may still be reading this rank's workspace (and
+        // this rank is done with theirs) when the mappings go away
+        int* d = reinterpret_cast<int*>(c->ws + c->L.ipc);
+        if (ncclAllReduce(d, d, 1, ncclInt32, ncclSum, c->comm, 0) == ncclSuccess) cudaStreamSynchronize(0);
+    }
+    for (void* p : c->peer_alloc)
+        if (p) cudaIpcCloseMemHandle(p);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->host_kx) cudaFreeHost(c->host_kx);
     delete c;

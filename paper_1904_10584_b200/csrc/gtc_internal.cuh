@@ -24,6 +24,13 @@ enum : unsigned long long {
     kFlagNonFinite = 1ull,  // a residual element was NaN/Inf
     kFlagCapacity = 2ull,   // the message did not fit max_words_per_rank
     kFlagCorrupt = 4ull,    // a caller-supplied message was not canonical
+    kFlagPeer = 8ull,       // a peer did not signal its message in time (p2p exchange)
+};
+
+// Header at the start of every message region (what peers read first).
+struct MsgHeader {
+    long long k;                  // words in the message
+    unsigned long long flags;     // the sender's sticky flags when it was packed
 };
 
 // Control block at the start of the workspace.  k and flags are adjacent so
@@ -53,6 +60,7 @@ struct EncodeParams {
     int* tile_cnt;           // [num_tiles] words per tile
     unsigned int* chunk_sum; // [num_chunks] words per chunk of kernel 1
     int* tile_off;           // [num_tiles + 1] exclusive word offsets per tile
+    MsgHeader* hdr;          // header of the message region (k, flags)
     Ctrl* ctrl;
     int num_tiles;
     int chunk_tiles;         // tiles per kernel-1 CTA (set by launch_encode)
@@ -78,6 +86,19 @@ struct DecodeParams {
     signed char* counts_out;   // may be null
     const unsigned long long* flags;  // skip everything if capacity/corrupt set
     int tiles_per_cta;         // set by launch_decode_apply
+    // p2p exchange (world > 1, peers' messages read over NVLink); ready == null otherwise
+    const MsgHeader* hdr[GTC_MAX_MSGS];  // every rank's header (peer pointers)
+    const unsigned long long* ready;     // [world] local flags, peer r writes ready[r] = epoch
+    unsigned long long epoch;            // this step's epoch
+    int self;                            // this rank (does not wait on itself)
+    unsigned long long* local_flags;     // remote flags are folded in here (Ctrl::flags)
+};
+
+struct SignalParams {
+    unsigned long long* peer_ready[GTC_MAX_MSGS];  // peer r's ready array (IPC-mapped)
+    int world;
+    int self;
+    unsigned long long epoch;
 };
 
 struct BoundsParams {
@@ -93,5 +114,6 @@ struct BoundsParams {
 cudaError_t launch_encode(const EncodeParams& p, int cmp_mode, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
+cudaError_t launch_signal(const SignalParams& p, cudaStream_t s);
 
 }  // namespace gtc

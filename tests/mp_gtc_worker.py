@@ -27,11 +27,13 @@ def main():
     n = int(os.environ.get("GTC_N", 1_000_003))
     steps = int(os.environ.get("GTC_STEPS", 4))
     cmp = os.environ.get("GTC_CMP", "gt")
+    exchange = os.environ.get("GTC_EXCHANGE", "p2p")
     tau = 8.0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=cmp)
+    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=cmp, exchange=exchange)
+    assert ctx.exchange_mode() == exchange, ctx.exchange_mode()
 
     r0 = [synth.uniform(n, -tau, tau, synth.rank_seed(w)) for w in range(world)]
     w0 = synth.normal(n, 99)
@@ -46,12 +48,13 @@ def main():
         ctx.encode(torch.from_numpy(gs[rank]).to(dev), rd)
         st = ctx.exchange()
         assert st == gtc.GTC_OK, st
+        assert ctx.check() == gtc.GTC_OK
         ctx.decode_apply(wd, -0.5, gtc.GTC_ACCUM_WEIGHTS, cnt)
         torch.cuda.synchronize()
         om, oc, _ = oracle.step(gs, r_or, w_or, tau, mode, -0.5, oracle.ACCUM_WEIGHTS)
         assert ctx.last_counts() == [m.size for m in om], (ctx.last_counts(), [m.size for m in om])
         for w in range(world):
-            got = ctx.message_tensor(w).cpu().numpy().view(np.uint32)
+            got = ctx.read_message(w)
             assert np.array_equal(got, om[w]), f"rank {rank} step {t}: message of rank {w}"
         assert np.array_equal(rd.cpu().numpy().view(np.uint32), r_or[rank].view(np.uint32)), "residual"
         assert np.array_equal(cnt.cpu().numpy().astype(np.int32), oc), "counts"
@@ -65,7 +68,7 @@ def main():
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
-        print(f"MULTIGPU OK world={world} n={n} steps={steps} cmp={cmp}")
+        print(f"MULTIGPU OK world={world} n={n} steps={steps} cmp={cmp} exchange={exchange}")
 
 
 if __name__ == "__main__":

@@ -17,10 +17,11 @@ def ngpus():
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("cmp", ["gt", "ge"])
-def test_nccl_exchange_parity(world, cmp):
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_exchange_parity(world, cmp, exchange):
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, GTC_CMP=cmp, GTC_STEPS="4", GTC_N="1000003")
+    env = dict(os.environ, GTC_CMP=cmp, GTC_STEPS="6", GTC_N="1000003", GTC_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
@@ -28,10 +29,11 @@ def test_nccl_exchange_parity(world, cmp):
     assert "MULTIGPU OK" in p.stdout
 
 
-def test_nccl_exchange_lstm_am_size():
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_exchange_lstm_am_size(exchange):
     if ngpus() < 2:
         pytest.skip("needs 2 GPUs")
-    env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="2", GTC_N="24286575")
+    env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="3", GTC_N="24286575", GTC_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29532", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
