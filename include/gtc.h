@@ -119,9 +119,14 @@ gtc_status gtc_get_unique_id(void* out_128_bytes);
 gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int world,
                     const void* nccl_unique_id, int cuda_device, uint32_t flags);
 
-/* Bytes of device workspace needed for messages of at most max_words_per_rank
- * words (<= 0 means n_params, which can never overflow) and for
- * gtc_decode_apply_msgs calls of up to max_sim_msgs messages (0 allowed). */
+/* Bytes of device workspace needed (include/gtc.h layout in gtc.cu):
+ *  - the segmented message of the hot path (per-tile slots, 4*n bytes, x2 in
+ *    p2p mode for step parity) -- it can never overflow;
+ *  - one contiguous message of at most max_words_per_rank words (<= 0 means
+ *    n_params): the wire format of the NCCL exchange (x world for the receive
+ *    buffer) and of gtc_message; a larger message there is GTC_ECAPACITY;
+ *  - tile offsets for gtc_decode_apply_msgs calls of up to max_sim_msgs
+ *    messages (0 allowed). */
 gtc_status gtc_workspace_size(const gtc_ctx* ctx, int64_t max_words_per_rank,
                               int max_sim_msgs, size_t* bytes);
 
@@ -136,13 +141,15 @@ gtc_status gtc_workspace_size(const gtc_ctx* ctx, int64_t max_words_per_rank,
 gtc_status gtc_bind_workspace(gtc_ctx* ctx, void* dev_ptr, size_t bytes,
                               int64_t max_words_per_rank, int max_sim_msgs);
 
-/* Steps 1-4 of P:222 for this rank, one fused kernel on `stream`.
+/* Steps 1-4 of P:222 for this rank: ONE fused streaming kernel on `stream`
+ * (residual accumulate, threshold, quantize, pack, per-tile compaction).
  *  grad     : float[n] device, read only; NULL means residual already holds
  *             residual + grad (the caller accumulated into it).
  *  residual : float[n] device, in/out; the caller zeroes it once at the start
  *             of training (R5) and checkpoints it with the weights.
- * The message (uint32 words, ascending index), its length k and per-tile
- * offsets stay in the workspace (see gtc_message / gtc_local_count). */
+ * The message stays in the workspace, segmented by tile: the packed words of
+ * tile t (ascending index) in slot t plus an epoch-stamped per-tile count.
+ * gtc_message / gtc_read_message pack it contiguously on demand. */
 gtc_status gtc_encode(gtc_ctx* ctx, const float* grad, float* residual, cudaStream_t stream);
 
 /* Make every rank's message available to every other rank (world > 1).

@@ -2,28 +2,40 @@
 // "The received sparse gradient updates are aggregated and weights are updated
 // based on the aggregate").
 //
-// One CTA per tiles_per_cta consecutive tiles of kTile params (the encode
-// tiling, so every message's slice for the CTA is [off[t0], off[t0+nt]) and its
-// reads are coalesced); tiles_per_cta is chosen so the grid is about one wave
-// of 8 CTAs per SM.
-//   1. counts c[0..kTile) in shared memory, int8 (|c| <= nmsg <= 64),
-//   2. ordered per-message passes: indices are unique within a message, so in
-//      one pass no two threads touch the same count; a barrier separates
-//      passes.  Integer sums: the result is independent of message order and
-//      needs no atomics (deterministic by construction, R6),
-//   3. sparse apply (R8): only elements with c != 0 are read-modify-written:
+// Messages come in two layouts (gtc_internal.cuh): SEGMENTED (the hot path:
+// words of tile t in slot t of a tile-major buffer, tag[t] = epoch<<32 |
+// count; in p2p mode the peers' buffers are read straight over NVLink) or
+// CONTIGUOUS (NCCL all-gather, caller messages: words + per-tile offsets).
+//
+// gtc_decode_apply_kernel (any number of messages):
+//   One CTA per tiles_per_cta consecutive tiles of kTile params; the grid is
+//   one wave of resident CTAs.  Per CTA:
+//   0. p2p: thread-parallel spin (acquire, system scope) on every rank's tags
+//      of the CTA's tiles until they carry this step's epoch -- the exchange
+//      is this tile-granular wait, overlapped with the other CTAs' work;
+//   1. counts c[0..span) in shared memory, int8 (|c| <= nmsg <= 64);
+//   2. ordered per-message passes over the CTA's words of each message:
+//      indices are unique within a message, so in one pass no two threads
+//      touch the same count; a barrier separates passes.  Integer sums: the
+//      result is independent of message order and needs no atomics
+//      (deterministic by construction, R6).  The first words of the
+//      first 8 messages are loaded into registers before the passes (one
+//      memory round trip);
+//   3. sparse apply (R8): only elements with c != 0 are read-modify-written,
 //        u = fl((float)c * tau);  WEIGHTS: t = fmaf(alpha, u, t);  UPDATE: t = fl(t + u)
-//      the non-zero counts of the CTA are compacted into a shared-memory list
-//      (per-thread 16-count masks from 128-bit shared loads, one block scan),
-//      then the list is applied by all threads: the target loads are all
-//      independent, one memory round trip per CTA.
-//   The first words of the first 8 messages are loaded into registers before
-//   the ordered passes, so the word reads also cost one round trip.
+//      via a shared-memory list of the non-zero counts (per-thread 16-count
+//      masks from 128-bit shared loads, one block scan), applied by all
+//      threads: the target loads are independent, one memory round trip;
 //   4. optional dense int8 counts dump (tests / parity only).
+// gtc_apply_single_*_kernel (one message, no counts dump): indices are
+//   unique, c = +-1 exactly on the message -- word-parallel, two round trips,
+//   no shared memory, no barriers.
 //
 // Algorithmic HBM bytes per launch: 4 * (sum of message words) (read) +
-// 4 * nmsg * (num_tiles + 1) (tile offsets) + 8 * |{i : c_i != 0}| (target RMW).
+// 8 * nmsg * num_tiles (tags) + 8 * |{i : c_i != 0}| (target RMW).
 #include "gtc_internal.cuh"
+
+#include <algorithm>
 
 namespace gtc {
 namespace {
@@ -33,16 +45,11 @@ constexpr int kPre = 2;                 // words per thread per message preloade
 constexpr int kPreMsgs = 8;             // messages whose first words are preloaded
 constexpr int kMaxTouched = 4096;       // non-zero counts applied through the list
 constexpr int kChunksPerThread = kDecMaxTilesPerCta * (kTile / 16) / kDecThreads;
+constexpr unsigned long long kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000;
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* a) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
     return v;
 }
 
@@ -52,51 +59,55 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-constexpr unsigned long long kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000;
-
-// p2p exchange gate (thread 0 of every CTA): wait until every peer has
-// published this step's message (ready[r] >= epoch: a peer can be at most one
-// step ahead, because its next decode waits for this rank's next signal),
-// then fold every rank's header flags.  Returns the flags; a capacity
-// overflow anywhere or a timed-out peer means nothing is applied anywhere.
-__device__ unsigned long long p2p_gate(const DecodeParams& p) {
-    unsigned long long f = 0;
-    const unsigned long long t0 = globaltimer_ns();
-    for (int r = 0; r < p.nmsg; ++r) {
-        if (r == p.self) continue;
-        while (ld_acquire_sys(&p.ready[r]) < p.epoch) {
-            if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
-                f |= kFlagPeer;
-                break;
-            }
-            __nanosleep(64);
+// Count of tile t of a segmented message; in p2p mode wait (acquire, system
+// scope) until the owner has published this step's tag.  Returns -1 on timeout.
+__device__ __forceinline__ int seg_count(const DecodeParams& p, int m, long long t) {
+    if (!p.wait) return (int)(__ldcg(p.tags[m] + t) & 0xffffffffull);
+    unsigned long long v = ld_acquire_sys(p.tags[m] + t);
+    if ((unsigned)(v >> 32) != p.epoch) {
+        const unsigned long long t0 = globaltimer_ns();
+        while ((unsigned)(v >> 32) != p.epoch) {
+            if (globaltimer_ns() - t0 > kPeerTimeoutNs) return -1;
+            __nanosleep(32);
+            v = ld_acquire_sys(p.tags[m] + t);
         }
-        if (f & kFlagPeer) break;
     }
-    if (!(f & kFlagPeer))
-        for (int r = 0; r < p.nmsg; ++r) f |= ld_relaxed_sys(&p.hdr[r]->flags);
-    return f;
+    return (int)(v & 0xffffffffull);
+}
+
+// Block 0 (segmented): this rank's word count = sum of its chunk sums.
+__device__ void total_words(const DecodeParams& p) {
+    __shared__ unsigned long long s_k[32];
+    unsigned long long k = 0;
+    for (int i = threadIdx.x; i < p.num_chunks; i += blockDim.x) k += __ldcg(p.chunk_sum + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(kFullMask, k, o);
+    if ((threadIdx.x & 31) == 0) s_k[threadIdx.x >> 5] = k;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_k[w];
+        *p.k_out = (long long)t;
+    }
 }
 
 template <int MODE>
+__device__ __forceinline__ void apply_one(const DecodeParams& p, long long gi, int c, float t) {
+    const float u = __fmul_rn((float)c, p.tau);
+    p.target[gi] = (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, u, t) : __fadd_rn(t, u);
+}
+
+template <int MODE, bool SEG>
 __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const DecodeParams p) {
     extern __shared__ int4 s_cnt4[];  // tiles_per_cta * kTile int8 counts
-    __shared__ int s_rng[GTC_MAX_MSGS][2];
+    __shared__ int s_beg[GTC_MAX_MSGS];                          // contiguous: first word
+    __shared__ int s_pre[GTC_MAX_MSGS][kDecMaxTilesPerCta + 1];  // words before tile i (per message)
     __shared__ unsigned s_warp[kDecThreads / 32];
     __shared__ unsigned short s_list[kMaxTouched];  // local indices with c != 0 (< 32768)
-    __shared__ unsigned long long s_gate;
+    __shared__ int s_abort;
 
+    if (SEG && blockIdx.x == 0 && p.k_out) total_words(p);
     if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;  // nothing is applied
-    if (p.ready) {
-        if (threadIdx.x == 0) {
-            const unsigned long long f = p2p_gate(p);
-            s_gate = f;
-            if (blockIdx.x == 0 && (f & (kFlagNonFinite | kFlagCapacity | kFlagPeer)))
-                atomicOr(p.local_flags, f & (kFlagNonFinite | kFlagCapacity | kFlagPeer));
-        }
-        __syncthreads();
-        if (s_gate & (kFlagCapacity | kFlagPeer)) return;
-    }
 
     signed char* s_cnt = reinterpret_cast<signed char*>(s_cnt4);
     const int tid = threadIdx.x;
@@ -105,15 +116,47 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     const int t0 = blockIdx.x * p.tiles_per_cta;
     const int nt = min(p.tiles_per_cta, p.num_tiles - t0);
     const long long base = (long long)t0 * kTile;
-    const int span = nt * kTile;
-    const int nq = span / 16;  // int4 chunks of 16 counts
+    const int nq = nt * (kTile / 16);  // int4 chunks of 16 counts
 
+    if (tid == 0) s_abort = 0;
     for (int q = tid; q < nq; q += kDecThreads) s_cnt4[q] = make_int4(0, 0, 0, 0);
-    for (int m = tid; m < p.nmsg; m += kDecThreads) {
-        s_rng[m][0] = __ldg(p.m.off[m] + t0);
-        s_rng[m][1] = __ldg(p.m.off[m] + t0 + nt);
+    __syncthreads();
+    if (SEG) {
+        // per (message, tile) counts; in p2p mode this is where the exchange waits
+        for (int idx = tid; idx < p.nmsg * nt; idx += kDecThreads) {
+            const int m = idx / nt, i = idx - m * nt;
+            const int c = seg_count(p, m, t0 + i);
+            if (c < 0) s_abort = 1;
+            s_pre[m][i + 1] = c < 0 ? 0 : c;
+        }
+        __syncthreads();
+        if (s_abort) {
+            if (tid == 0) atomicOr(p.flags, kFlagPeer);
+            return;
+        }
+        for (int m = tid; m < p.nmsg; m += kDecThreads) {  // exclusive prefix over the CTA's tiles
+            s_pre[m][0] = 0;
+            for (int i = 1; i <= nt; ++i) s_pre[m][i] += s_pre[m][i - 1];
+        }
+    } else {
+        for (int m = tid; m < p.nmsg; m += kDecThreads) {
+            const int b = __ldg(p.off[m] + t0);
+            s_beg[m] = b;
+            s_pre[m][0] = 0;
+            s_pre[m][nt] = __ldg(p.off[m] + t0 + nt) - b;
+        }
     }
     __syncthreads();
+
+    // the f-th word of message m among this CTA's words
+    auto word_at = [&](int m, int f) -> unsigned {
+        if (SEG) {
+            int i = 0;
+            while (i + 1 < nt && f >= s_pre[m][i + 1]) ++i;
+            return __ldcg(p.seg[m] + (long long)(t0 + i) * kTile + (f - s_pre[m][i]));
+        }
+        return __ldg(p.words[m] + s_beg[m] + f);
+    };
 
     // preload the first words of the first messages (one memory round trip)
     unsigned pre[kPreMsgs][kPre];
@@ -121,40 +164,38 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     for (int m = 0; m < kPreMsgs; ++m) {
 #pragma unroll
         for (int u = 0; u < kPre; ++u) {
+            pre[m][u] = 0u;
             if (m < p.nmsg) {
-                const int j = s_rng[m][0] + u * kDecThreads + tid;
-                pre[m][u] = j < s_rng[m][1] ? __ldg(p.m.words[m] + j) : 0u;
+                const int f = u * kDecThreads + tid;
+                if (f < s_pre[m][nt]) pre[m][u] = word_at(m, f);
             }
         }
     }
 
-    // ordered per-message passes; indices are unique within a message, so no
-    // two threads of one pass touch the same count (no atomics)
+    // ordered per-message passes
 #pragma unroll
     for (int m = 0; m < kPreMsgs; ++m) {
         if (m >= p.nmsg) break;
-        const int b = s_rng[m][0], e = s_rng[m][1];
+        const int len = s_pre[m][nt];
 #pragma unroll
         for (int u = 0; u < kPre; ++u) {
-            if (b + u * kDecThreads + tid < e) {
+            if (u * kDecThreads + tid < len) {
                 const unsigned word = pre[m][u];
                 const int local = (int)((word >> 1) - (unsigned)base);
                 s_cnt[local] = (signed char)(s_cnt[local] + ((word & 1u) ? -1 : 1));
             }
         }
-        const unsigned* w = p.m.words[m];
-        for (int j = b + kPre * kDecThreads + tid; j < e; j += kDecThreads) {
-            const unsigned word = __ldg(w + j);
+        for (int f = kPre * kDecThreads + tid; f < len; f += kDecThreads) {
+            const unsigned word = word_at(m, f);
             const int local = (int)((word >> 1) - (unsigned)base);
             s_cnt[local] = (signed char)(s_cnt[local] + ((word & 1u) ? -1 : 1));
         }
         __syncthreads();
     }
     for (int m = kPreMsgs; m < p.nmsg; ++m) {
-        const unsigned* w = p.m.words[m];
-        const int e = s_rng[m][1];
-        for (int j = s_rng[m][0] + tid; j < e; j += kDecThreads) {
-            const unsigned word = __ldg(w + j);
+        const int len = s_pre[m][nt];
+        for (int f = tid; f < len; f += kDecThreads) {
+            const unsigned word = word_at(m, f);
             const int local = (int)((word >> 1) - (unsigned)base);
             s_cnt[local] = (signed char)(s_cnt[local] + ((word & 1u) ? -1 : 1));
         }
@@ -176,9 +217,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         }
     }
 
-    // sparse apply: compact the non-zero counts of the whole CTA into one list
-    // (block scan, no atomics), then every thread applies list entries -- all
-    // target loads are independent: one memory round trip per CTA
+    // sparse apply through a list of the non-zero counts
     unsigned nz[kChunksPerThread];
     unsigned my = 0;
 #pragma unroll
@@ -229,11 +268,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         for (unsigned i = tid; i < total; i += kDecThreads) {
             const int local = s_list[i];
             const long long gi = base + local;
-            if (gi < p.n) {
-                const float t = p.target[gi];
-                const float u = __fmul_rn((float)s_cnt[local], p.tau);
-                p.target[gi] = (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, u, t) : __fadd_rn(t, u);
-            }
+            if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
         }
     } else {
         // dense batch: each thread applies its own chunks
@@ -246,11 +281,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
                 msk &= msk - 1;
                 const int local = q * 16 + b;
                 const long long gi = base + local;
-                if (gi < p.n) {
-                    const float t = p.target[gi];
-                    const float uu = __fmul_rn((float)s_cnt[local], p.tau);
-                    p.target[gi] = (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, uu, t) : __fadd_rn(t, uu);
-                }
+                if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
             }
         }
     }
@@ -258,39 +289,57 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
 
 // One message (world == 1, or one simulated worker): indices are unique, so
 // c[i] = +-1 exactly on the message's indices and 0 elsewhere; the aggregate
-// needs no counts at all.  Word-parallel: each thread loads 4 words, then the
-// 4 targets, then stores -- two memory round trips, no shared memory, no
-// barriers.  fl(+-1 * tau) = +-tau exactly, so the arithmetic is the general
-// kernel's (R8).  The message length is read on the device (tile_off[num_tiles]).
+// needs no counts.  fl(+-1 * tau) = +-tau exactly, so the arithmetic is the
+// general kernel's (R8).  Loads are batched (4 per thread) before the stores.
 constexpr int kSingleThreads = 256;
 constexpr int kSingleBatch = 4;
 
 template <int MODE>
-__global__ void __launch_bounds__(kSingleThreads) gtc_apply_single_kernel(const DecodeParams p) {
-    if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;
-    const long long k = __ldg(p.m.off[0] + p.num_tiles);
-    const unsigned* words = p.m.words[0];
-    const long long stride = (long long)gridDim.x * kSingleThreads * kSingleBatch;
-    for (long long j0 = (long long)blockIdx.x * kSingleThreads * kSingleBatch + threadIdx.x; j0 < k; j0 += stride) {
-        unsigned w[kSingleBatch];
+__device__ __forceinline__ void apply_words(const DecodeParams& p, const unsigned* w, int cnt, int lane,
+                                            int stride) {
+    for (int j0 = 0; j0 < cnt; j0 += stride * kSingleBatch) {
+        unsigned wd[kSingleBatch];
         float t[kSingleBatch];
 #pragma unroll
         for (int u = 0; u < kSingleBatch; ++u) {
-            const long long j = j0 + u * kSingleThreads;
-            w[u] = j < k ? __ldg(words + j) : 0u;
+            const int j = j0 + u * stride + lane;
+            wd[u] = j < cnt ? __ldcg(w + j) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < kSingleBatch; ++u)
-            if (j0 + u * kSingleThreads < k) t[u] = p.target[w[u] >> 1];
+            if (j0 + u * stride + lane < cnt) t[u] = p.target[wd[u] >> 1];
 #pragma unroll
         for (int u = 0; u < kSingleBatch; ++u) {
-            if (j0 + u * kSingleThreads < k) {
-                const float q = (w[u] & 1u) ? -p.tau : p.tau;  // fl(c * tau) for c = -1 / +1
-                p.target[w[u] >> 1] = (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, q, t[u])
-                                                                  : __fadd_rn(t[u], q);
+            if (j0 + u * stride + lane < cnt) {
+                const float q = (wd[u] & 1u) ? -p.tau : p.tau;  // fl(c * tau) for c = -1 / +1
+                p.target[wd[u] >> 1] = (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, q, t[u])
+                                                                   : __fadd_rn(t[u], q);
             }
         }
     }
+}
+
+// segmented: one warp per tile
+template <int MODE>
+__global__ void __launch_bounds__(kSingleThreads) gtc_apply_single_seg_kernel(const DecodeParams p) {
+    if (blockIdx.x == 0 && p.k_out) total_words(p);
+    if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * (kSingleThreads / 32);
+    for (long long t = (long long)blockIdx.x * (kSingleThreads / 32) + warp; t < p.num_tiles; t += stride) {
+        const int cnt = (int)(__ldcg(p.tags[0] + t) & 0xffffffffull);
+        if (cnt) apply_words<MODE>(p, p.seg[0] + t * kTile, cnt, lane, 32);
+    }
+}
+
+// contiguous: word-parallel over the whole message (length from off[num_tiles])
+template <int MODE>
+__global__ void __launch_bounds__(kSingleThreads) gtc_apply_single_kernel(const DecodeParams p) {
+    if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;
+    const long long k = __ldg(p.off[0] + p.num_tiles);
+    const long long per = (long long)kSingleThreads * kSingleBatch;
+    for (long long j0 = (long long)blockIdx.x * per; j0 < k; j0 += (long long)gridDim.x * per)
+        apply_words<MODE>(p, p.words[0] + j0, (int)min(per, k - j0), threadIdx.x, kSingleThreads);
 }
 
 // Tile offsets of caller-supplied messages (gtc_decode_apply_msgs): for every
@@ -327,55 +376,59 @@ __global__ void gtc_tile_bounds_kernel(const BoundsParams p) {
     if (bad) atomicOr(p.flags, kFlagCorrupt);
 }
 
-}  // namespace
-
-cudaError_t launch_decode_apply(const DecodeParams& p_in, int accum_mode, cudaStream_t s) {
-    if (p_in.num_tiles == 0) return cudaSuccess;
+int sm_count() {
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) return e;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
     }
-    if (p_in.nmsg == 1 && p_in.counts_out == nullptr) {
-        const int grid = sms * 8;
-        if (accum_mode == GTC_ACCUM_UPDATE)
-            gtc_apply_single_kernel<GTC_ACCUM_UPDATE><<<grid, kSingleThreads, 0, s>>>(p_in);
-        else
-            gtc_apply_single_kernel<GTC_ACCUM_WEIGHTS><<<grid, kSingleThreads, 0, s>>>(p_in);
-        return cudaGetLastError();
-    }
-    // about one wave of 8 CTAs per SM, at most kDecMaxTilesPerCta tiles per CTA
+    return sms;
+}
+
+template <int MODE, bool SEG>
+cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
+    auto kern = gtc_decode_apply_kernel<MODE, SEG>;
+    static int resident[kDecMaxTilesPerCta + 1] = {0};
     DecodeParams p = p_in;
-    int tpc = (p.num_tiles + sms * 8 - 1) / (sms * 8);
-    tpc = tpc < 1 ? 1 : (tpc > kDecMaxTilesPerCta ? kDecMaxTilesPerCta : tpc);
+    const int sms = sm_count();
+    // smallest tiles_per_cta whose grid fits in one wave of resident CTAs
+    int tpc = 1;
+    for (; tpc <= kDecMaxTilesPerCta; ++tpc) {
+        if (resident[tpc] == 0) {
+            int r = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kDecThreads, (size_t)tpc * kTile) != cudaSuccess)
+                r = 1;
+            resident[tpc] = r < 1 ? 1 : r;
+        }
+        if ((long long)(p.num_tiles + tpc - 1) / tpc <= (long long)resident[tpc] * sms) break;
+    }
+    if (tpc > kDecMaxTilesPerCta) tpc = kDecMaxTilesPerCta;
     p.tiles_per_cta = tpc;
     const int grid = (p.num_tiles + tpc - 1) / tpc;
-    const size_t smem = (size_t)tpc * kTile;
-    if (accum_mode == GTC_ACCUM_UPDATE)
-        gtc_decode_apply_kernel<GTC_ACCUM_UPDATE><<<grid, kDecThreads, smem, s>>>(p);
-    else
-        gtc_decode_apply_kernel<GTC_ACCUM_WEIGHTS><<<grid, kDecThreads, smem, s>>>(p);
+    kern<<<grid, kDecThreads, (size_t)tpc * kTile, s>>>(p);
     return cudaGetLastError();
 }
 
-// p2p exchange: publish "this rank's message of step `epoch` is ready" into
-// every peer's ready[self] (remote store over NVLink, release at system scope
-// after a system fence; the message itself was written by the preceding
-// encode kernels on the same stream).
-__global__ void gtc_signal_kernel(const SignalParams p) {
-    const int r = threadIdx.x;
-    if (r < p.world && r != p.self) {
-        __threadfence_system();
-        unsigned long long* a = p.peer_ready[r] + p.self;
-        asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(a), "l"(p.epoch) : "memory");
+template <int MODE>
+cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
+    if (p.nmsg == 1 && p.counts_out == nullptr && !p.wait) {
+        if (p.segmented) {
+            const int grid = (int)std::min<long long>((p.num_tiles + 7) / 8, (long long)sm_count() * 8);
+            gtc_apply_single_seg_kernel<MODE><<<grid, kSingleThreads, 0, s>>>(p);
+        } else {
+            gtc_apply_single_kernel<MODE><<<sm_count() * 8, kSingleThreads, 0, s>>>(p);
+        }
+        return cudaGetLastError();
     }
+    return p.segmented ? launch_general<MODE, true>(p, s) : launch_general<MODE, false>(p, s);
 }
 
-cudaError_t launch_signal(const SignalParams& p, cudaStream_t s) {
-    gtc_signal_kernel<<<1, 64, 0, s>>>(p);
-    return cudaGetLastError();
+}  // namespace
+
+cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s) {
+    if (p.num_tiles == 0) return cudaSuccess;
+    return accum_mode == GTC_ACCUM_UPDATE ? launch_mode<GTC_ACCUM_UPDATE>(p, s) : launch_mode<GTC_ACCUM_WEIGHTS>(p, s);
 }
 
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s) {

@@ -8,10 +8,9 @@
 // and the selected words are compacted, in ascending index order (R4), into
 // one contiguous message.  HBM-bound: no contraction, no tensor cores.
 //
-// Kernel 1, gtc_encode_tiles_kernel (the streaming pass, ~all of the bytes):
-//   - persistent, 2 CTAs x 256 threads per SM; CTA b owns a contiguous chunk
-//     of tiles (kTile = 4096 params each): no CTA ever waits for another, so
-//     there is no residency requirement and no look-back chain;
+// Kernel 1, gtc_encode_tiles_kernel (the whole hot-path encode):
+//   - persistent, 2 CTAs x 512 threads per SM; CTA b owns a contiguous chunk
+//     of tiles (kTile = 4096 params each): no CTA ever waits for another;
 //   - thread 0 keeps kStages tiles in flight with 1-D TMA bulk copies
 //     (cp.async.bulk.shared::cluster.global.mbarrier::complete_tx) of r and g
 //     into shared memory; the CTA reads its stage with conflict-free 128-bit
@@ -20,18 +19,19 @@
 //     ascending index; intra-tile ranks come from three __ballot_sync/__popc
 //     per round (a thread holds <= 4 words per round) and one 32-entry warp
 //     scan over the (round, warp) totals;
-//   - the tile's words go, compacted, to its slot of a tile-major scratch; its
-//     count to tile_cnt[]; the chunk's count to chunk_sum[b] at the end.
-// Kernel 2, gtc_compact_kernel (reads/writes ~8*rho B/param): one warp per
-//   tile; a CTA sums the chunk sums of earlier chunks and the counts of the
-//   earlier tiles of its chunk (all loads independent), derives its tiles'
-//   global offsets and copies the words into the message.
-// Every count is rewritten every call: no atomics, no memset, no host state
-// (the pair is CUDA-graph capturable).
+//   - the tile's words go, compacted, to slot t of the segmented message and
+//     its tag (epoch << 32 | count) is published after them (one tile later,
+//     behind the next block barrier; release at system scope when peers read
+//     it over NVLink); the chunk's word count goes to chunk_sum[b].
+// Kernel 2, gtc_compact_kernel (on demand: NCCL exchange, gtc_message): one
+//   warp per tile turns a segmented message (this rank's, or a peer's over
+//   NVLink) into the contiguous wire format: global tile offsets (sum of
+//   earlier chunks + earlier tiles of the chunk, all loads independent) and
+//   the words copied in order.
+// No atomics, no memset, no state carried between calls except the epoch.
 //
 // HBM bytes per parameter (algorithmic): 4 (read g) + 4 (read r) + 4 (write r)
-// + 4*rho (write words); + 4 B per tile (offsets).  The scratch round trip
-// adds 8*rho (0.08 B/param at rho = 1 %).
+// + 4*rho (write words); + 8 B per tile (tag).
 #include "gtc_internal.cuh"
 
 #include <mutex>
@@ -44,6 +44,7 @@ constexpr int kStages = 3;                       // TMA pipeline depth per CTA
 constexpr int kTileBytes = kTile * 4;             // 16 KB per tensor per tile
 constexpr int kVec4PerTile = kTile / 4;           // float4 per tensor per tile
 constexpr int kCompactThreads = 256;
+constexpr int kMaxChunkTiles = 2048;              // 2^31 params = 524288 tiles over 256+ chunks
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -124,6 +125,7 @@ template <int CMP, bool HAS_G>
 __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const EncodeParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<HAS_G>& sm = *reinterpret_cast<Smem<HAS_G>*>(smem_raw);
+    unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw + sizeof(Smem<HAS_G>));  // [chunk_tiles]
     __shared__ __align__(8) unsigned long long full[kStages];
     __shared__ unsigned s_scan[kEncVec * kEncWarps];
     __shared__ unsigned s_total;
@@ -235,15 +237,16 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
             s_scan[lane] = incl - x;
             if (lane == 31) {
                 s_total = incl;
-                p.tile_cnt[tile] = (int)incl;
+                s_cnt[it] = incl;
                 chunk_total += incl;
             }
         }
         __syncthreads();  // tile-local offsets known
 
-        // ---- pack and store the words, compacted, in the tile's scratch slot
-        if (s_total != 0) {
-            unsigned* dst = p.scratch + base;
+        // ---- pack and store the words, compacted, in the tile's slot
+        const unsigned total = s_total;
+        if (total != 0) {
+            unsigned* dst = p.seg + base;
 #pragma unroll
             for (int j = 0; j < kEncVec; ++j) {
                 unsigned o = s_scan[j * kEncWarps + warp] + my_off[j];
@@ -258,13 +261,31 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
             }
         }
     }
+    // Publish the chunk: every word of every tile is written (barrier), then
+    // one thread fences (system scope when peers read over NVLink) and stamps
+    // the tiles' tags; a reader that sees tag[t] with this epoch sees tile t.
+    __syncthreads();
+    if (tid == 0) {
+        if (p.publish_sys) __threadfence_system();
+        for (long long t = t_begin; t < t_end; ++t) {
+            const unsigned long long v = make_tag(p.epoch, s_cnt[t - t_begin]);
+            if (p.publish_sys)
+                asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p.tags + t), "l"(v) : "memory");
+            else
+                p.tags[t] = v;
+        }
+    }
     if (tid == 31) p.chunk_sum[blockIdx.x] = chunk_total;
 }
 
 // Kernel 2: one warp per tile, kCompactWarps tiles per CTA.
 constexpr int kCompactWarps = kCompactThreads / 32;
 
-__global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const EncodeParams p) {
+__device__ __forceinline__ unsigned tag_count(const unsigned long long* tags, long long t) {
+    return (unsigned)(__ldcg(tags + t) & 0xffffffffull);
+}
+
+__global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const CompactParams p) {
     __shared__ unsigned s_red[kCompactWarps];
     __shared__ unsigned s_cnt[kCompactWarps];
 
@@ -280,8 +301,8 @@ __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const Enco
     // words before this CTA: earlier chunks + earlier tiles of its chunk
     unsigned part = 0;
     for (int i = tid; i < c; i += kCompactThreads) part += __ldcg(p.chunk_sum + i);
-    for (int i = t_chunk + tid; i < t_cta; i += kCompactThreads) part += (unsigned)__ldcg(p.tile_cnt + i);
-    const unsigned my_cnt = has_tile ? (unsigned)__ldcg(p.tile_cnt + tile) : 0u;
+    for (int i = t_chunk + tid; i < t_cta; i += kCompactThreads) part += tag_count(p.tags, i);
+    const unsigned my_cnt = has_tile ? tag_count(p.tags, tile) : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
     if (lane == 0) {
@@ -313,7 +334,7 @@ __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const Enco
             p.hdr->flags = f;
         }
     }
-    const unsigned* src = p.scratch + (long long)tile * kTile;
+    const unsigned* src = p.seg + (long long)tile * kTile;
     for (unsigned j0 = 0; j0 < my_cnt; j0 += 4 * 32) {
         unsigned w[4];
 #pragma unroll
@@ -334,7 +355,8 @@ cudaError_t launch_tiles(EncodeParams& p, cudaStream_t s) {
     static std::once_flag once;
     static int per_sm = 0, sms = 0;
     static cudaError_t init_err = cudaSuccess;
-    const size_t smem = sizeof(Smem<HAS_G>);
+    // + per-tile counts of the chunk (<= kMaxChunkTiles: n < 2^31 over >= 256 chunks)
+    const size_t smem = sizeof(Smem<HAS_G>) + sizeof(unsigned) * kMaxChunkTiles;
     auto kern = gtc_encode_tiles_kernel<CMP, HAS_G>;
     std::call_once(once, [&] {
         init_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -351,7 +373,9 @@ cudaError_t launch_tiles(EncodeParams& p, cudaStream_t s) {
     if (grid > kMaxChunks) grid = kMaxChunks;
     if (grid > p.num_tiles) grid = p.num_tiles;
     p.chunk_tiles = (p.num_tiles + grid - 1) / grid;
+    if (p.chunk_tiles > kMaxChunkTiles) p.chunk_tiles = kMaxChunkTiles;
     p.num_chunks = (p.num_tiles + p.chunk_tiles - 1) / p.chunk_tiles;
+    if (p.num_chunks > kMaxChunks) return cudaErrorInvalidValue;
     kern<<<p.num_chunks, kEncThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -363,11 +387,13 @@ cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t launch_encode(const EncodeParams& p_in, int cmp_mode, cudaStream_t s) {
-    if (p_in.num_tiles == 0) return cudaSuccess;
-    EncodeParams p = p_in;
-    cudaError_t e = cmp_mode == GTC_CMP_GE ? launch_cmp<GTC_CMP_GE>(p, s) : launch_cmp<GTC_CMP_GT>(p, s);
-    if (e != cudaSuccess) return e;
+cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s) {
+    if (p.num_tiles == 0) return cudaSuccess;
+    return cmp_mode == GTC_CMP_GE ? launch_cmp<GTC_CMP_GE>(p, s) : launch_cmp<GTC_CMP_GT>(p, s);
+}
+
+cudaError_t launch_compact(const CompactParams& p, cudaStream_t s) {
+    if (p.num_tiles == 0) return cudaSuccess;
     gtc_compact_kernel<<<(p.num_tiles + kCompactWarps - 1) / kCompactWarps, kCompactThreads, 0, s>>>(p);
     return cudaGetLastError();
 }

@@ -3,15 +3,18 @@
 // worker communicates the sparse update to all other workers and conversely
 // receives all sparse updates from other workers").
 //
-// Two exchange modes for world > 1:
+// The hot-path message is segmented (gtc_internal.cuh): encode writes each
+// tile's packed words into that tile's slot and publishes a per-tile tag.
+// Exchange modes for world > 1:
 //   p2p  (default): every rank's workspace is mapped into its peers with CUDA
-//        IPC at bind time.  gtc_exchange launches a one-warp signal kernel that
-//        publishes "message of step e ready" into every peer's ready[] array
-//        over NVLink; gtc_decode_apply reads every rank's header, tile offsets
-//        and words straight from the owner's memory over NVLink.  No host sync,
-//        no staging copy; messages are double-buffered by step parity.
-//   nccl (GTC_EXCHANGE_NCCL): ncclAllGather of (k, flags), one host wait for
-//        the largest k, then ncclAllGather of the words and tile offsets.
+//        IPC at bind time; decode_apply reads every rank's tags and words for
+//        its tiles straight from the owner's memory over NVLink, waiting per
+//        tile on the owner's tag (epoch-stamped, release/acquire at system
+//        scope).  No host sync, no collective launch, no staging copy; the
+//        segmented buffers are double-buffered by step parity.
+//   nccl (GTC_EXCHANGE_NCCL): the message is packed contiguously, then
+//        ncclAllGather of (k, flags), one host wait for the largest k,
+//        ncclAllGather of the words and tile offsets.
 #include <nccl.h>
 
 #include <algorithm>
@@ -32,61 +35,49 @@ enum class Stage { kBound, kEncoded, kExchanged };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// A message region: header | tile offsets | words.  Same layout on every rank.
-struct Region {
-    size_t hdr, tile_off, words, bytes;
-};
-
-Region make_region(long long tiles, long long capacity) {
-    Region R{};
-    size_t o = 0;
-    R.hdr = o;      o = align_up(o + sizeof(MsgHeader), 256);
-    R.tile_off = o; o = align_up(o + sizeof(int) * (size_t)(tiles + 1), 256);
-    R.words = o;    o = align_up(o + sizeof(unsigned) * (size_t)std::max(capacity, 1LL), 256);
-    R.bytes = o;
-    return R;
-}
-
 // Workspace layout (offsets from the bound base, each 256-byte aligned):
-//   ctrl      Ctrl                              k, flags
-//   chunk_sum u32[kMaxChunks]                   words per encode-kernel-1 chunk
-//   tile_cnt  i32[num_tiles]                    words per tile
-//   scratch   u32[num_tiles * kTile]            tile-major words (encode kernel 1)
-//   region    Region x (1, or 2 for p2p)        header | tile offsets | words
-//   ready     u64[world]                        p2p: written by peers over NVLink
-//   ipc       128 B x world                     p2p: bind-time handle exchange
-//   kx_all    i64[2 * world]                    nccl: all-gathered (k, flags)
-//   recv      u32[world * capacity]             nccl: all-gathered messages
-//   recv_off  i32[world * (num_tiles + 1)]      nccl: all-gathered tile offsets
-//   sim_off   i32[max_sim_msgs * (num_tiles+1)] tile offsets for decode_apply_msgs
+//   ctrl      Ctrl                               k, flags
+//   chunk_sum u32[kMaxChunks]                    words per encode chunk
+//   seg[p]    { u64 tags[T] | u32 words[T*kTile] } segmented message, p < nseg
+//                                                (nseg = 2 in p2p mode: step parity)
+//   msg       { MsgHeader | i32 tile_off[T+1] | u32 words[capacity] }
+//                                                contiguous message (NCCL / on demand)
+//   ipc       128 B x world                      bind-time IPC records (world > 1)
+//   kx_all    i64[2 * world]                     nccl: all-gathered (k, flags)
+//   recv      u32[world * capacity]              nccl: all-gathered messages
+//   recv_off  i32[world * (T + 1)]               nccl: all-gathered tile offsets
+//   sim_off   i32[max_sim_msgs * (T + 1)]        tile offsets for decode_apply_msgs
 struct Layout {
-    Region R;
-    int nregions;
-    size_t ctrl, chunk_sum, tile_cnt, scratch, region[2], ready, ipc, kx_all, recv, recv_off, sim_off, total;
+    int nseg;
+    size_t ctrl, chunk_sum, seg_tags[2], seg_words[2];
+    size_t msg_hdr, msg_off, msg_words;
+    size_t ipc, kx_all, recv, recv_off, sim_off, total;
 };
 
 constexpr size_t kIpcRecord = 128;
 
 Layout make_layout(long long n, int world, bool p2p, long long capacity, int max_sim_msgs) {
     const long long tiles = (n + kTile - 1) / kTile;
+    const size_t T = (size_t)std::max(tiles, 1LL);
     Layout L{};
     size_t o = 0;
     L.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
     L.chunk_sum = o; o = align_up(o + sizeof(unsigned) * (size_t)kMaxChunks, 256);
-    L.tile_cnt = o;  o = align_up(o + sizeof(int) * (size_t)std::max(tiles, 1LL), 256);
-    L.scratch = o;   o = align_up(o + sizeof(unsigned) * (size_t)std::max(tiles, 1LL) * kTile, 256);
-    L.R = make_region(tiles, capacity);
-    L.nregions = (world > 1 && p2p) ? 2 : 1;
+    L.nseg = (world > 1 && p2p) ? 2 : 1;
     for (int i = 0; i < 2; ++i) {
-        L.region[i] = o;
-        if (i < L.nregions) o += L.R.bytes;
+        L.seg_tags[i] = L.seg_words[i] = 0;
+        if (i >= L.nseg) continue;
+        L.seg_tags[i] = o;  o = align_up(o + sizeof(unsigned long long) * T, 256);
+        L.seg_words[i] = o; o = align_up(o + sizeof(unsigned) * T * kTile, 256);
     }
-    L.ready = L.ipc = L.kx_all = L.recv = L.recv_off = 0;
-    if (world > 1 && p2p) {
-        L.ready = o; o = align_up(o + sizeof(unsigned long long) * (size_t)world, 256);
-        L.ipc = o;   o = align_up(o + kIpcRecord * (size_t)world, 256);
-    } else if (world > 1) {
-        L.ipc = o;      o = align_up(o + kIpcRecord * (size_t)world, 256);
+    L.msg_hdr = o;   o = align_up(o + sizeof(MsgHeader), 256);
+    L.msg_off = o;   o = align_up(o + sizeof(int) * (size_t)(tiles + 1), 256);
+    L.msg_words = o; o = align_up(o + sizeof(unsigned) * (size_t)std::max(capacity, 1LL), 256);
+    L.ipc = L.kx_all = L.recv = L.recv_off = 0;
+    if (world > 1) {
+        L.ipc = o; o = align_up(o + kIpcRecord * (size_t)world, 256);
+    }
+    if (world > 1 && !p2p) {
         L.kx_all = o;   o = align_up(o + sizeof(long long) * 2 * (size_t)world, 256);
         L.recv = o;     o = align_up(o + sizeof(unsigned) * (size_t)world * (size_t)std::max(capacity, 1LL), 256);
         L.recv_off = o; o = align_up(o + sizeof(int) * (size_t)world * (size_t)(tiles + 1), 256);
@@ -123,18 +114,17 @@ struct gtc_ctx {
     Layout L{};
 
     Ctrl* ctrl = nullptr;
-    unsigned* chunk_sum = nullptr;
-    int* tile_cnt = nullptr;
-    unsigned* scratch = nullptr;
     long long* kx_all = nullptr;
     unsigned* recv = nullptr;
     int* recv_off = nullptr;
     int* sim_off = nullptr;
 
-    // p2p: every rank's workspace base as seen from this process (self = ws)
+    // every rank's workspace base as seen from this process (self = ws)
     std::vector<unsigned char*> peer_ws;
     std::vector<void*> peer_alloc;  // what cudaIpcOpenMemHandle returned (to close)
-    unsigned long long epoch = 0;   // p2p step counter; parity selects the region
+    unsigned epoch = 0;             // step counter: tag stamp; parity selects the p2p buffer
+    int chunk_tiles = 1, num_chunks = 1;  // encode chunking of the last launch (same on all ranks)
+    int packed_rank = -1;           // whose message the contiguous region holds (-1: stale)
 
     long long* host_kx = nullptr;  // pinned, 2 * world
     std::vector<long long> last_k;
@@ -183,13 +173,12 @@ gtc_status flags_to_status(unsigned long long f) {
     return GTC_OK;
 }
 
-// The region (of this rank or a peer) a step's message lives in.
-unsigned char* region_base(const gtc_ctx* c, int rank, int parity) {
-    unsigned char* base = (c->world > 1 && c->p2p) ? c->peer_ws[rank] : c->ws;
-    return base + c->L.region[parity];
-}
+int seg_parity(const gtc_ctx* c) { return c->L.nseg == 2 ? (int)(c->epoch & 1u) : 0; }
 
-int cur_parity(const gtc_ctx* c) { return (c->world > 1 && c->p2p) ? (int)(c->epoch & 1ull) : 0; }
+// workspace base of `rank` as seen from this process
+unsigned char* rank_ws(const gtc_ctx* c, int rank) {
+    return (c->world > 1 && c->p2p) ? c->peer_ws[rank] : c->ws;
+}
 
 // Base address of the allocation holding p (driver API, resolved at run time
 // so that libgtc.so does not link libcuda).
@@ -214,7 +203,8 @@ bool allocation_base(const void* p, unsigned long long* base) {
 gtc_status connect_peers(gtc_ctx* c) {
     IpcRecord rec{};
     unsigned long long base = 0;
-    rec.ok = allocation_base(c->ws, &base) && cudaIpcGetMemHandle(&rec.handle, reinterpret_cast<void*>(base)) == cudaSuccess;
+    rec.ok = allocation_base(c->ws, &base) &&
+             cudaIpcGetMemHandle(&rec.handle, reinterpret_cast<void*>(base)) == cudaSuccess;
     cudaGetLastError();
     rec.offset = rec.ok ? reinterpret_cast<unsigned long long>(c->ws) - base : 0ull;
     rec.total = c->L.total;
@@ -272,6 +262,35 @@ gtc_status connect_peers(gtc_ctx* c) {
         return fail(c, GTC_EUNSUPPORTED,
                     "p2p exchange: workspaces cannot be mapped across ranks (use GTC_EXCHANGE_NCCL)");
     }
+    return GTC_OK;
+}
+
+// Pack rank `rank`'s segmented message of the current step into this rank's
+// contiguous region (header, tile offsets, words).
+gtc_status pack_contiguous(gtc_ctx* c, int rank, cudaStream_t stream) {
+    unsigned char* src = rank_ws(c, rank);
+    const int par = seg_parity(c);
+    CompactParams q{};
+    q.seg = reinterpret_cast<const unsigned*>(src + c->L.seg_words[par]);
+    q.tags = reinterpret_cast<const unsigned long long*>(src + c->L.seg_tags[par]);
+    q.chunk_sum = reinterpret_cast<const unsigned*>(src + c->L.chunk_sum);
+    q.chunk_tiles = c->chunk_tiles;
+    q.num_tiles = c->num_tiles;
+    q.words = reinterpret_cast<unsigned*>(c->ws + c->L.msg_words);
+    q.tile_off = reinterpret_cast<int*>(c->ws + c->L.msg_off);
+    q.hdr = reinterpret_cast<MsgHeader*>(c->ws + c->L.msg_hdr);
+    q.capacity = c->capacity;
+    q.ctrl = c->ctrl;
+    if (c->num_tiles == 0) {
+        cudaError_t e = cudaMemsetAsync(c->ws + c->L.msg_hdr, 0, sizeof(MsgHeader), stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + c->L.msg_off, 0, sizeof(int), stream);
+        if (e != cudaSuccess) return cuda_fail(c, e, "pack: n == 0");
+    } else {
+        cudaError_t e = launch_compact(q, stream);
+        if (e != cudaSuccess) return cuda_fail(c, e, "pack: launch");
+        c->launches += 1;
+    }
+    c->packed_rank = rank;
     return GTC_OK;
 }
 
@@ -372,12 +391,12 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     if (bytes < L.total) return fail(c, GTC_EINVAL, "workspace too small");
     DeviceGuard g(c->device);
     unsigned char* b = static_cast<unsigned char*>(dev_ptr);
-    // Control block, chunk sums and counts start at 0; so do the region
-    // headers/offsets and the p2p ready flags.
-    cudaError_t e = cudaMemset(b, 0, L.scratch);
-    for (int i = 0; i < L.nregions && e == cudaSuccess; ++i)
-        e = cudaMemset(b + L.region[i], 0, L.R.words);
-    if (e == cudaSuccess && c->world > 1 && c->p2p) e = cudaMemset(b + L.ready, 0, L.ipc - L.ready);
+    // control block, chunk sums, tags (epoch 0 = never published) and the
+    // contiguous header/offsets start at 0
+    cudaError_t e = cudaMemset(b, 0, L.chunk_sum + sizeof(unsigned) * kMaxChunks);
+    for (int i = 0; i < L.nseg && e == cudaSuccess; ++i)
+        e = cudaMemset(b + L.seg_tags[i], 0, L.seg_words[i] - L.seg_tags[i]);
+    if (e == cudaSuccess) e = cudaMemset(b + L.msg_hdr, 0, L.msg_words - L.msg_hdr);
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: cudaMemset");
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: sync");
@@ -387,9 +406,6 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     c->max_sim_msgs = max_sim_msgs;
     c->L = L;
     c->ctrl = reinterpret_cast<Ctrl*>(b + L.ctrl);
-    c->chunk_sum = reinterpret_cast<unsigned*>(b + L.chunk_sum);
-    c->tile_cnt = reinterpret_cast<int*>(b + L.tile_cnt);
-    c->scratch = reinterpret_cast<unsigned*>(b + L.scratch);
     if (c->world > 1 && !c->p2p) {
         c->kx_all = reinterpret_cast<long long*>(b + L.kx_all);
         c->recv = reinterpret_cast<unsigned*>(b + L.recv);
@@ -416,42 +432,40 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     if (!aligned16(residual) || !aligned16(grad)) return fail(c, GTC_EALIGN, "encode: grad/residual alignment");
     DeviceGuard g(c->device);
 
-    c->epoch += 1;  // p2p: this step's epoch; its parity picks the message region
-    unsigned char* reg = region_base(c, c->rank, cur_parity(c));
-    MsgHeader* hdr = reinterpret_cast<MsgHeader*>(reg + c->L.R.hdr);
-    int* tile_off = reinterpret_cast<int*>(reg + c->L.R.tile_off);
-
+    c->epoch = c->epoch == 0xffffffffu ? 1u : c->epoch + 1u;  // 0 is never a published stamp
+    c->packed_rank = -1;
     if (c->num_tiles == 0) {  // n == 0: empty message
         cudaError_t e = cudaMemsetAsync(&c->ctrl->k, 0, sizeof(long long), stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(hdr, 0, sizeof(MsgHeader), stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(tile_off, 0, sizeof(int), stream);
         if (e != cudaSuccess) return cuda_fail(c, e, "encode: n == 0");
         c->stage = Stage::kEncoded;
         return GTC_OK;
     }
-
+    const int par = seg_parity(c);
     EncodeParams p{};
     p.g = grad;
     p.r = residual;
     p.n = c->n;
     p.tau = c->tau;
-    p.words = reinterpret_cast<unsigned*>(reg + c->L.R.words);
-    p.capacity = c->capacity;
-    p.scratch = c->scratch;
-    p.tile_cnt = c->tile_cnt;
-    p.chunk_sum = c->chunk_sum;
-    p.tile_off = tile_off;
-    p.hdr = hdr;
+    p.seg = reinterpret_cast<unsigned*>(c->ws + c->L.seg_words[par]);
+    p.tags = reinterpret_cast<unsigned long long*>(c->ws + c->L.seg_tags[par]);
+    p.chunk_sum = reinterpret_cast<unsigned*>(c->ws + c->L.chunk_sum);
     p.ctrl = c->ctrl;
+    p.epoch = c->epoch;
+    p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     p.num_tiles = c->num_tiles;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "encode: launch");
-    c->launches += 2;
+    c->chunk_tiles = p.chunk_tiles;
+    c->num_chunks = p.num_chunks;
+    c->launches += 1;
     c->stage = Stage::kEncoded;
     return GTC_OK;
 }
 
 static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
+    // 0. the wire format: this rank's message, contiguous
+    gtc_status s = pack_contiguous(c, c->rank, stream);
+    if (s != GTC_OK) return s;
     // 1. (k, flags) of every rank.  Ctrl::k and Ctrl::flags are adjacent.
     ncclResult_t r = ncclAllGather(&c->ctrl->k, c->kx_all, 2, ncclInt64, c->comm, stream);
     if (r != ncclSuccess) return nccl_fail(c, r, "exchange: ncclAllGather(counts)");
@@ -483,13 +497,11 @@ static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
     }
     c->max_k = max_k;
     // 3. words (padded to the largest k) and tile offsets, one NCCL group.
-    unsigned char* reg = c->ws + c->L.region[0];
     r = ncclGroupStart();
     if (r == ncclSuccess && max_k > 0)
-        r = ncclAllGather(reg + c->L.R.words, c->recv, (size_t)max_k, ncclUint32, c->comm, stream);
+        r = ncclAllGather(c->ws + c->L.msg_words, c->recv, (size_t)max_k, ncclUint32, c->comm, stream);
     if (r == ncclSuccess)
-        r = ncclAllGather(reg + c->L.R.tile_off, c->recv_off, (size_t)c->num_tiles + 1, ncclInt32, c->comm,
-                          stream);
+        r = ncclAllGather(c->ws + c->L.msg_off, c->recv_off, (size_t)c->num_tiles + 1, ncclInt32, c->comm, stream);
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess) return nccl_fail(c, r, "exchange: ncclAllGather(words)");
     if (r2 != ncclSuccess) return nccl_fail(c, r2, "exchange: ncclGroupEnd");
@@ -501,24 +513,15 @@ static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
 gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
     if (!c) return GTC_EINVAL;
     if (c->stage != Stage::kEncoded) return fail(c, GTC_ESTATE, "exchange: no encode since the last exchange");
-    if (c->world == 1) {
+    if (c->world == 1 || c->p2p) {
+        // world 1: nothing to send.  p2p: the encode kernel already published
+        // every tile (epoch-stamped tags); decode_apply reads the peers'
+        // tiles in place over NVLink as they become ready.
         c->stage = Stage::kExchanged;
         return GTC_OK;
     }
     DeviceGuard g(c->device);
-    if (!c->p2p) return exchange_nccl(c, stream);
-    // p2p: publish "step epoch ready" into every peer's ready[rank]
-    SignalParams sp{};
-    for (int i = 0; i < c->world; ++i)
-        sp.peer_ready[i] = reinterpret_cast<unsigned long long*>(c->peer_ws[i] + c->L.ready);
-    sp.world = c->world;
-    sp.self = c->rank;
-    sp.epoch = c->epoch;
-    cudaError_t e = launch_signal(sp, stream);
-    if (e != cudaSuccess) return cuda_fail(c, e, "exchange: signal launch");
-    c->launches += 1;
-    c->stage = Stage::kExchanged;
-    return GTC_OK;
+    return exchange_nccl(c, stream);
 }
 
 static gtc_status check_apply_args(gtc_ctx* c, float* target, int mode) {
@@ -536,24 +539,24 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     if (s != GTC_OK) return s;
     DeviceGuard g(c->device);
     DecodeParams p{};
-    const int par = cur_parity(c);
     if (c->world == 1 || c->p2p) {
+        const int par = seg_parity(c);
+        p.segmented = 1;
         for (int i = 0; i < c->world; ++i) {
-            unsigned char* reg = region_base(c, i, par);
-            p.m.words[i] = reinterpret_cast<const unsigned*>(reg + c->L.R.words);
-            p.m.off[i] = reinterpret_cast<const int*>(reg + c->L.R.tile_off);
-            p.hdr[i] = reinterpret_cast<const MsgHeader*>(reg + c->L.R.hdr);
+            unsigned char* b = rank_ws(c, i);
+            p.seg[i] = reinterpret_cast<const unsigned*>(b + c->L.seg_words[par]);
+            p.tags[i] = reinterpret_cast<const unsigned long long*>(b + c->L.seg_tags[par]);
         }
-        if (c->world > 1) {
-            p.ready = reinterpret_cast<const unsigned long long*>(c->ws + c->L.ready);
-            p.epoch = c->epoch;
-            p.self = c->rank;
-            p.local_flags = &c->ctrl->flags;
-        }
+        p.epoch = c->epoch;
+        p.wait = c->world > 1 ? 1 : 0;
+        p.chunk_sum = reinterpret_cast<const unsigned*>(c->ws + c->L.chunk_sum);
+        p.num_chunks = c->num_chunks;
+        p.k_out = &c->ctrl->k;
     } else {
+        p.segmented = 0;
         for (int i = 0; i < c->world; ++i) {
-            p.m.words[i] = c->recv + (size_t)i * (size_t)c->max_k;
-            p.m.off[i] = c->recv_off + (size_t)i * (size_t)(c->num_tiles + 1);
+            p.words[i] = c->recv + (size_t)i * (size_t)c->max_k;
+            p.off[i] = c->recv_off + (size_t)i * (size_t)(c->num_tiles + 1);
         }
     }
     p.nmsg = c->world;
@@ -606,8 +609,8 @@ gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const 
         b.words[m] = msgs[m] ? msgs[m] : &kEmpty;
         b.k[m] = counts[m];
         b.off[m] = c->sim_off + (size_t)m * (size_t)(c->num_tiles + 1);
-        p.m.words[m] = b.words[m];
-        p.m.off[m] = b.off[m];
+        p.words[m] = b.words[m];
+        p.off[m] = b.off[m];
     }
     b.nmsg = nmsg;
     b.n = c->n;
@@ -616,6 +619,7 @@ gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const 
     e = launch_tile_bounds(b, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "decode_apply_msgs: bounds launch");
     if (nmsg > 0) c->launches += 1;
+    p.segmented = 0;
     p.nmsg = nmsg;
     p.n = c->n;
     p.num_tiles = c->num_tiles;
@@ -647,6 +651,27 @@ gtc_status gtc_local_count(const gtc_ctx* c, const int64_t** dev_k) {
     return GTC_OK;
 }
 
+// Contiguous copy of `rank`'s message of the current step in this rank's
+// contiguous region (packs it if needed); waits for the device.
+static gtc_status contiguous_message(gtc_ctx* c, int rank, const uint32_t** dev_words, int64_t* k) {
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "message: sync");
+    if (c->packed_rank != rank) {
+        gtc_status s = pack_contiguous(c, rank, 0);
+        if (s != GTC_OK) return s;
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(c, e, "message: pack");
+    }
+    MsgHeader h{};
+    e = cudaMemcpy(&h, c->ws + c->L.msg_hdr, sizeof(h), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "message: header");
+    if (h.k > c->capacity) return fail(c, GTC_ECAPACITY, "message: larger than max_words_per_rank");
+    *dev_words = reinterpret_cast<const uint32_t*>(c->ws + c->L.msg_words);
+    *k = h.k;
+    return GTC_OK;
+}
+
 gtc_status gtc_last_counts(gtc_ctx* c, int64_t* k_per_rank) {
     if (!c || !k_per_rank) return GTC_EINVAL;
     if (!c->bound) return fail(c, GTC_ESTATE, "last_counts: workspace not bound");
@@ -656,12 +681,19 @@ gtc_status gtc_last_counts(gtc_ctx* c, int64_t* k_per_rank) {
     }
     DeviceGuard g(c->device);
     cudaError_t e = cudaDeviceSynchronize();
-    for (int i = 0; i < c->world && e == cudaSuccess; ++i) {
-        MsgHeader h{};
-        e = cudaMemcpy(&h, region_base(c, i, cur_parity(c)) + c->L.R.hdr, sizeof(h), cudaMemcpyDeviceToHost);
-        k_per_rank[i] = h.k;
+    if (e != cudaSuccess) return cuda_fail(c, e, "last_counts: sync");
+    // sum of every rank's chunk sums of the last encode
+    for (int i = 0; i < c->world; ++i) {
+        std::vector<unsigned> cs(c->num_chunks, 0u);
+        if (c->num_tiles > 0) {
+            e = cudaMemcpy(cs.data(), rank_ws(c, i) + c->L.chunk_sum, sizeof(unsigned) * c->num_chunks,
+                           cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return cuda_fail(c, e, "last_counts: readback");
+        }
+        long long k = 0;
+        for (unsigned v : cs) k += v;
+        k_per_rank[i] = k;
     }
-    if (e != cudaSuccess) return cuda_fail(c, e, "last_counts: readback");
     return GTC_OK;
 }
 
@@ -674,12 +706,7 @@ gtc_status gtc_message(gtc_ctx* c, int rank, const uint32_t** dev_words, int64_t
         *k = c->last_k[rank];
         return GTC_OK;
     }
-    std::vector<int64_t> ks(c->world);
-    gtc_status s = gtc_last_counts(c, ks.data());
-    if (s != GTC_OK) return s;
-    *dev_words = reinterpret_cast<const uint32_t*>(region_base(c, rank, cur_parity(c)) + c->L.R.words);
-    *k = ks[rank];
-    return GTC_OK;
+    return contiguous_message(c, rank, dev_words, k);
 }
 
 gtc_status gtc_read_message(gtc_ctx* c, int rank, uint32_t* host_words, int64_t max_words, int64_t* k) {

@@ -22,83 +22,91 @@ static_assert(kTile == kDecThreads * 16, "decode sweep assumes 16 counts per thr
 // Sticky device flags (Ctrl::flags).
 enum : unsigned long long {
     kFlagNonFinite = 1ull,  // a residual element was NaN/Inf
-    kFlagCapacity = 2ull,   // the message did not fit max_words_per_rank
+    kFlagCapacity = 2ull,   // a contiguous message did not fit max_words_per_rank
     kFlagCorrupt = 4ull,    // a caller-supplied message was not canonical
-    kFlagPeer = 8ull,       // a peer did not signal its message in time (p2p exchange)
-};
-
-// Header at the start of every message region (what peers read first).
-struct MsgHeader {
-    long long k;                  // words in the message
-    unsigned long long flags;     // the sender's sticky flags when it was packed
+    kFlagPeer = 8ull,       // a peer did not publish a tile in time (p2p exchange)
 };
 
 // Control block at the start of the workspace.  k and flags are adjacent so
-// one 16-byte all-gather carries both.
+// one 16-byte all-gather carries both (NCCL mode).
 struct alignas(256) Ctrl {
-    long long k;                  // words of the last encode
+    long long k;                  // words of the last encode (set by compaction / decode)
     unsigned long long flags;     // sticky flags
 };
 
-// Encode runs as two kernels (encode.cu):
-//   1. gtc_encode_tiles_kernel: CTA b streams a contiguous chunk of
-//      chunk_tiles tiles of g and r, writes r, compacts each tile's words into
-//      its slot of a tile-major scratch, writes the tile's word count and, at
-//      the end, its chunk's word count (every entry rewritten every call: no
-//      atomics, no zeroing, no state carried between calls);
-//   2. gtc_compact_kernel: one warp per tile turns the counts into global tile
-//      offsets (sum of earlier chunks + earlier tiles of its chunk) and copies
-//      the words into the contiguous message.
+// Header of a contiguous message region.
+struct MsgHeader {
+    long long k;
+    unsigned long long flags;
+};
+
+// ---------------------------------------------------------------- messages
+// The hot path's message is SEGMENTED: encode kernel 1 compacts the words of
+// tile t (ascending index) into slot t of a tile-major buffer,
+//     words of tile t = seg[t * kTile .. t * kTile + count_t),
+// and publishes tag[t] = (epoch << 32) | count_t after them (release at system
+// scope when peers read it over NVLink).  Decode reads exactly the words of
+// the tiles it owns, from every rank, without a global prefix scan.
+// The CONTIGUOUS message (words in one array + per-tile offsets + header) is
+// the wire format of the NCCL exchange and of gtc_message; gtc_compact_kernel
+// builds it from a segmented one on demand.
+inline __host__ __device__ unsigned long long make_tag(unsigned epoch, unsigned count) {
+    return ((unsigned long long)epoch << 32) | count;
+}
+
 struct EncodeParams {
-    const float* g;          // may be null (residual already holds r + g)
+    const float* g;                // may be null (residual already holds r + g)
     float* r;
     long long n;
     float tau;
-    unsigned int* words;     // message out (contiguous)
-    long long capacity;      // words available
-    unsigned int* scratch;   // [num_tiles * kTile] tile-major words
-    int* tile_cnt;           // [num_tiles] words per tile
-    unsigned int* chunk_sum; // [num_chunks] words per chunk of kernel 1
-    int* tile_off;           // [num_tiles + 1] exclusive word offsets per tile
-    MsgHeader* hdr;          // header of the message region (k, flags)
+    unsigned int* seg;             // [num_tiles * kTile] tile-major words
+    unsigned long long* tags;      // [num_tiles] (epoch << 32) | count
+    unsigned int* chunk_sum;       // [num_chunks] words per kernel-1 chunk
     Ctrl* ctrl;
+    unsigned epoch;
+    int publish_sys;               // peers read the tags: release at system scope
     int num_tiles;
-    int chunk_tiles;         // tiles per kernel-1 CTA (set by launch_encode)
-    int num_chunks;          // kernel-1 grid (set by launch_encode)
+    int chunk_tiles;               // tiles per kernel-1 CTA (set by launch_encode)
+    int num_chunks;                // kernel-1 grid (set by launch_encode)
 };
 
 // Most kernel-1 CTAs (chunks) a launch may use: 148 SMs x 2, with headroom.
 constexpr int kMaxChunks = 1024;
 
-struct MsgSet {
-    const unsigned int* words[GTC_MAX_MSGS];
-    const int* off[GTC_MAX_MSGS];  // per message: [num_tiles + 1] tile offsets
+struct CompactParams {             // segmented (any rank) -> contiguous (local)
+    const unsigned int* seg;
+    const unsigned long long* tags;
+    const unsigned int* chunk_sum;
+    int chunk_tiles;
+    int num_tiles;
+    unsigned int* words;
+    int* tile_off;                 // [num_tiles + 1]
+    MsgHeader* hdr;
+    long long capacity;
+    Ctrl* ctrl;                    // local: k and the capacity flag
 };
 
 struct DecodeParams {
-    MsgSet m;
+    int segmented;                 // 1: seg/tags (hot path), 0: words/off (contiguous)
+    const unsigned int* words[GTC_MAX_MSGS];       // contiguous
+    const int* off[GTC_MAX_MSGS];                  // contiguous: [num_tiles + 1] tile offsets
+    const unsigned int* seg[GTC_MAX_MSGS];         // segmented (peer pointers in p2p)
+    const unsigned long long* tags[GTC_MAX_MSGS];  // segmented
+    unsigned epoch;                // segmented: tags of this step
+    int wait;                      // segmented: spin until a tag carries this epoch (p2p)
     int nmsg;
     long long n;
     int num_tiles;
     float tau;
     float alpha;
     float* target;
-    signed char* counts_out;   // may be null
-    const unsigned long long* flags;  // skip everything if capacity/corrupt set
-    int tiles_per_cta;         // set by launch_decode_apply
-    // p2p exchange (world > 1, peers' messages read over NVLink); ready == null otherwise
-    const MsgHeader* hdr[GTC_MAX_MSGS];  // every rank's header (peer pointers)
-    const unsigned long long* ready;     // [world] local flags, peer r writes ready[r] = epoch
-    unsigned long long epoch;            // this step's epoch
-    int self;                            // this rank (does not wait on itself)
-    unsigned long long* local_flags;     // remote flags are folded in here (Ctrl::flags)
-};
-
-struct SignalParams {
-    unsigned long long* peer_ready[GTC_MAX_MSGS];  // peer r's ready array (IPC-mapped)
-    int world;
-    int self;
-    unsigned long long epoch;
+    signed char* counts_out;       // may be null
+    unsigned long long* flags;     // this rank's Ctrl::flags
+    int tiles_per_cta;             // set by launch_decode_apply
+    // segmented: block 0 also totals this rank's chunk sums into *k_out
+    const unsigned int* chunk_sum;
+    int num_chunks;
+    long long* k_out;
 };
 
 struct BoundsParams {
@@ -111,9 +119,9 @@ struct BoundsParams {
     unsigned long long* flags;
 };
 
-cudaError_t launch_encode(const EncodeParams& p, int cmp_mode, cudaStream_t s);
+cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s);
+cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
-cudaError_t launch_signal(const SignalParams& p, cudaStream_t s);
 
 }  // namespace gtc

@@ -308,7 +308,10 @@ def test_error_paths():
         gtc.gtc_init(10, 0.0)
 
 
-def test_capacity_overflow_reported_and_nothing_applied():
+def test_capacity_bounds_only_the_contiguous_message():
+    """The hot path's segmented message cannot overflow: the step applies in
+    full; max_words_per_rank bounds only the contiguous wire format, which
+    reports GTC_ECAPACITY when asked for."""
     n, tau = 100_000, 1.0
     ctx = gtc.GTC(n, tau, max_words_per_rank=100)
     v = synth.normal(n, 13) * np.float32(3.0)
@@ -316,9 +319,17 @@ def test_capacity_overflow_reported_and_nothing_applied():
     w = torch.zeros(n, device=DEV)
     ctx.encode(None, rd)
     ctx.exchange()
-    ctx.decode_apply(w)
-    assert ctx.check() == gtc.GTC_ECAPACITY
-    assert torch.count_nonzero(w).item() == 0
+    ctx.decode_apply(w, 1.0, gtc.GTC_ACCUM_UPDATE)
+    assert ctx.check() == gtc.GTC_OK
+    r_host = v.copy()
+    words, _ = oracle.encode(None, r_host, tau)
+    w_exp = np.zeros(n, np.float32)
+    oracle.apply(oracle.decode_counts([words], n), w_exp, tau, 1.0, oracle.ACCUM_UPDATE)
+    assert_float_parity(w.cpu().numpy(), w_exp, "update")
+    assert ctx.last_counts() == [words.size]
+    with pytest.raises(gtc.GTCError) as e:
+        ctx.message()
+    assert e.value.status == gtc.GTC_ECAPACITY
     ctx.close()
 
 
