@@ -75,11 +75,11 @@ __device__ __forceinline__ int seg_count(const DecodeParams& p, int m, long long
     return (int)(v & 0xffffffffull);
 }
 
-// Block 0 (segmented): this rank's word count = sum of its chunk sums.
+// Block 0 (segmented): this rank's word count = sum of its tile counts.
 __device__ void total_words(const DecodeParams& p) {
     __shared__ unsigned long long s_k[32];
     unsigned long long k = 0;
-    for (int i = threadIdx.x; i < p.num_chunks; i += blockDim.x) k += __ldcg(p.chunk_sum + i);
+    for (int i = threadIdx.x; i < p.num_tiles; i += blockDim.x) k += __ldcg(p.own_tags + i) & 0xffffffffull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(kFullMask, k, o);
     if ((threadIdx.x & 31) == 0) s_k[threadIdx.x >> 5] = k;

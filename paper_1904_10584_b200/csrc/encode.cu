@@ -34,6 +34,8 @@
 // + 4*rho (write words); + 8 B per tile (tag).
 #include "gtc_internal.cuh"
 
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 namespace gtc {
@@ -145,7 +147,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
     __syncthreads();
     const float tau = p.tau;
     const unsigned lt = lanemask_lt();
-    unsigned chunk_total = 0;  // meaningful in warp 0, lane 31
 
     int it = 0;
     for (long long tile = t_begin; tile < t_end; ++tile, ++it) {
@@ -238,7 +239,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
             if (lane == 31) {
                 s_total = incl;
                 s_cnt[it] = incl;
-                chunk_total += incl;
             }
         }
         __syncthreads();  // tile-local offsets known
@@ -275,16 +275,180 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
                 p.tags[t] = v;
         }
     }
-    if (tid == 31) p.chunk_sum[blockIdx.x] = chunk_total;
 }
 
-// Kernel 2: one warp per tile, kCompactWarps tiles per CTA.
+// One tile per CTA (the default variant): 256 threads, four 128-bit loads of
+// r and four of g per thread issued before any use, 4 CTAs per SM; no shared
+// state between CTAs.  Same arithmetic and word order as the persistent
+// variant above.
+constexpr int kTileThreads = 256;
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kTileVec = kTile / (kTileThreads * 4);  // 4
+static_assert(kTileVec * kTileWarps == 32, "one (round, warp) scan entry per lane");
+
+__device__ __forceinline__ float4 ld_nc_v4(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ float4 ld_v4(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+template <int CMP, bool HAS_G>
+__global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const EncodeParams p) {
+    __shared__ unsigned s_scan[kTileVec * kTileWarps];
+    __shared__ unsigned s_total;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const long long tile = blockIdx.x;
+    const long long base = tile * kTile;
+    const bool full_tile = base + kTile <= p.n;
+
+    float4 rv[kTileVec];
+    float4 gv[kTileVec];
+    if (full_tile) {
+        const float4* r4 = reinterpret_cast<const float4*>(p.r + base);
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) rv[j] = ld_v4(r4 + j * kTileThreads + tid);
+        if (HAS_G) {
+            const float4* g4 = reinterpret_cast<const float4*>(p.g + base);
+#pragma unroll
+            for (int j = 0; j < kTileVec; ++j) gv[j] = ld_nc_v4(g4 + j * kTileThreads + tid);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const long long i = base + (long long)(j * kTileThreads + tid) * 4 + e;
+                set_comp(rv[j], e, i < p.n ? p.r[i] : 0.0f);
+                if (HAS_G) set_comp(gv[j], e, i < p.n ? p.g[i] : 0.0f);
+            }
+        }
+    }
+
+    const float tau = p.tau;
+    unsigned sel = 0u, neg = 0u;
+    bool nonfinite = false;
+#pragma unroll
+    for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float v = HAS_G ? __fadd_rn(comp(rv[j], e), comp(gv[j], e)) : comp(rv[j], e);
+            const float a = fabsf(v);
+            nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
+            const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
+            const bool ng = v < 0.0f;
+            const float rn = sl ? (ng ? __fadd_rn(v, tau) : __fsub_rn(v, tau)) : v;
+            set_comp(rv[j], e, rn);
+            sel |= (unsigned)sl << (j * 4 + e);
+            neg |= (unsigned)(sl && ng) << (j * 4 + e);
+        }
+    }
+
+    if (full_tile) {
+        float4* r4 = reinterpret_cast<float4*>(p.r + base);
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) st_stream(r4 + j * kTileThreads + tid, rv[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const long long i = base + (long long)(j * kTileThreads + tid) * 4 + e;
+                if (i < p.n) p.r[i] = comp(rv[j], e);
+            }
+        }
+    }
+    if (__any_sync(kFull, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
+
+    const unsigned lt = lanemask_lt();
+    unsigned my_off[kTileVec];
+#pragma unroll
+    for (int j = 0; j < kTileVec; ++j) {
+        const unsigned c = __popc((sel >> (4 * j)) & 0xfu);  // 0..4
+        const unsigned b0 = __ballot_sync(kFull, c & 1u);
+        const unsigned b1 = __ballot_sync(kFull, c & 2u);
+        const unsigned b2 = __ballot_sync(kFull, c & 4u);
+        my_off[j] = __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+        if (lane == 0) s_scan[j * kTileWarps + warp] = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned x = s_scan[lane];
+        unsigned incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        s_scan[lane] = incl - x;
+        if (lane == 31) {
+            s_total = incl;
+            if (!p.publish_sys) p.tags[tile] = make_tag(p.epoch, incl);  // read by later kernels only
+        }
+    }
+    __syncthreads();
+    const unsigned total = s_total;
+    if (total != 0) {
+        unsigned* dst = p.seg + base;
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+            unsigned o = s_scan[j * kTileWarps + warp] + my_off[j];
+            const unsigned i0 = (unsigned)(base + (long long)(j * kTileThreads + tid) * 4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if ((sel >> (4 * j + e)) & 1u) {
+                    dst[o] = ((i0 + e) << 1) | ((neg >> (4 * j + e)) & 1u);
+                    ++o;
+                }
+            }
+        }
+    }
+    if (p.publish_sys) {  // peers read this tile over NVLink: words first, then the tag
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p.tags + tile), "l"(make_tag(p.epoch, total))
+                         : "memory");
+        }
+    }
+}
+
+// Kernel 2 (packing, on demand): group sums of kGroupTiles tile counts, one
+// warp per group.
 constexpr int kCompactWarps = kCompactThreads / 32;
+static_assert(kGroupTiles % kCompactWarps == 0, "a compact CTA never straddles a group");
 
 __device__ __forceinline__ unsigned tag_count(const unsigned long long* tags, long long t) {
     return (unsigned)(__ldcg(tags + t) & 0xffffffffull);
 }
 
+__global__ void __launch_bounds__(kCompactThreads) gtc_group_sums_kernel(const CompactParams p) {
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * kCompactWarps + (threadIdx.x >> 5);
+    const int ng = (p.num_tiles + kGroupTiles - 1) / kGroupTiles;
+    if (g >= ng) return;
+    unsigned s = 0;
+    for (int t = g * kGroupTiles + lane; t < min((g + 1) * kGroupTiles, p.num_tiles); t += 32)
+        s += tag_count(p.tags, t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) p.group_sum[g] = s;
+}
+
+// Kernel 3 (packing, on demand): one warp per tile, kCompactWarps tiles per
+// CTA.  A CTA's global prefix = group sums of all earlier groups + counts of
+// the earlier tiles of its group (all loads independent); each warp copies its
+// tile's words (loads batched before stores).
 __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const CompactParams p) {
     __shared__ unsigned s_red[kCompactWarps];
     __shared__ unsigned s_cnt[kCompactWarps];
@@ -293,15 +457,14 @@ __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const Comp
     const int lane = tid & 31;
     const int warp = tid >> 5;
     const int t_cta = blockIdx.x * kCompactWarps;      // first tile of this CTA
-    const int c = t_cta / p.chunk_tiles;               // its kernel-1 chunk
-    const int t_chunk = c * p.chunk_tiles;             // first tile of that chunk
+    const int g = t_cta / kGroupTiles;                 // its group
+    const int t_grp = g * kGroupTiles;                 // first tile of that group
     const int tile = t_cta + warp;
     const bool has_tile = tile < p.num_tiles;
 
-    // words before this CTA: earlier chunks + earlier tiles of its chunk
     unsigned part = 0;
-    for (int i = tid; i < c; i += kCompactThreads) part += __ldcg(p.chunk_sum + i);
-    for (int i = t_chunk + tid; i < t_cta; i += kCompactThreads) part += tag_count(p.tags, i);
+    for (int i = tid; i < g; i += kCompactThreads) part += __ldcg(p.group_sum + i);
+    for (int i = t_grp + tid; i < t_cta; i += kCompactThreads) part += tag_count(p.tags, i);
     const unsigned my_cnt = has_tile ? tag_count(p.tags, tile) : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
@@ -380,9 +543,29 @@ cudaError_t launch_tiles(EncodeParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int CMP, bool HAS_G>
+cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
+    p.chunk_tiles = 1;
+    p.num_chunks = p.num_tiles;
+    gtc_encode_tile_kernel<CMP, HAS_G><<<p.num_tiles, kTileThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+// Encode variant: one tile per CTA (default) or the persistent TMA pipeline
+// (GTC_ENCODE_VARIANT=persistent, kept for measurement).
+bool use_persistent() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_ENCODE_VARIANT");
+        v = (e && std::strcmp(e, "persistent") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 template <int CMP>
 cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
-    return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
+    if (use_persistent()) return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
+    return p.g ? launch_tile<CMP, true>(p, s) : launch_tile<CMP, false>(p, s);
 }
 
 }  // namespace
@@ -394,6 +577,8 @@ cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s) {
 
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s) {
     if (p.num_tiles == 0) return cudaSuccess;
+    const int ng = (p.num_tiles + kGroupTiles - 1) / kGroupTiles;
+    gtc_group_sums_kernel<<<(ng + kCompactWarps - 1) / kCompactWarps, kCompactThreads, 0, s>>>(p);
     gtc_compact_kernel<<<(p.num_tiles + kCompactWarps - 1) / kCompactWarps, kCompactThreads, 0, s>>>(p);
     return cudaGetLastError();
 }

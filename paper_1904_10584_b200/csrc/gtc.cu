@@ -37,7 +37,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the bound base, each 256-byte aligned):
 //   ctrl      Ctrl                               k, flags
-//   chunk_sum u32[kMaxChunks]                    words per encode chunk
+//   group_sum u32[ceil(T / kGroupTiles)]         packing scratch
 //   seg[p]    { u64 tags[T] | u32 words[T*kTile] } segmented message, p < nseg
 //                                                (nseg = 2 in p2p mode: step parity)
 //   msg       { MsgHeader | i32 tile_off[T+1] | u32 words[capacity] }
@@ -49,7 +49,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 //   sim_off   i32[max_sim_msgs * (T + 1)]        tile offsets for decode_apply_msgs
 struct Layout {
     int nseg;
-    size_t ctrl, chunk_sum, seg_tags[2], seg_words[2];
+    size_t ctrl, group_sum, seg_tags[2], seg_words[2];
     size_t msg_hdr, msg_off, msg_words;
     size_t ipc, kx_all, recv, recv_off, sim_off, total;
 };
@@ -62,7 +62,7 @@ Layout make_layout(long long n, int world, bool p2p, long long capacity, int max
     Layout L{};
     size_t o = 0;
     L.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
-    L.chunk_sum = o; o = align_up(o + sizeof(unsigned) * (size_t)kMaxChunks, 256);
+    L.group_sum = o; o = align_up(o + sizeof(unsigned) * ((T + kGroupTiles - 1) / kGroupTiles), 256);
     L.nseg = (world > 1 && p2p) ? 2 : 1;
     for (int i = 0; i < 2; ++i) {
         L.seg_tags[i] = L.seg_words[i] = 0;
@@ -123,7 +123,6 @@ struct gtc_ctx {
     std::vector<unsigned char*> peer_ws;
     std::vector<void*> peer_alloc;  // what cudaIpcOpenMemHandle returned (to close)
     unsigned epoch = 0;             // step counter: tag stamp; parity selects the p2p buffer
-    int chunk_tiles = 1, num_chunks = 1;  // encode chunking of the last launch (same on all ranks)
     int packed_rank = -1;           // whose message the contiguous region holds (-1: stale)
 
     long long* host_kx = nullptr;  // pinned, 2 * world
@@ -273,8 +272,7 @@ gtc_status pack_contiguous(gtc_ctx* c, int rank, cudaStream_t stream) {
     CompactParams q{};
     q.seg = reinterpret_cast<const unsigned*>(src + c->L.seg_words[par]);
     q.tags = reinterpret_cast<const unsigned long long*>(src + c->L.seg_tags[par]);
-    q.chunk_sum = reinterpret_cast<const unsigned*>(src + c->L.chunk_sum);
-    q.chunk_tiles = c->chunk_tiles;
+    q.group_sum = reinterpret_cast<unsigned*>(c->ws + c->L.group_sum);
     q.num_tiles = c->num_tiles;
     q.words = reinterpret_cast<unsigned*>(c->ws + c->L.msg_words);
     q.tile_off = reinterpret_cast<int*>(c->ws + c->L.msg_off);
@@ -288,7 +286,7 @@ gtc_status pack_contiguous(gtc_ctx* c, int rank, cudaStream_t stream) {
     } else {
         cudaError_t e = launch_compact(q, stream);
         if (e != cudaSuccess) return cuda_fail(c, e, "pack: launch");
-        c->launches += 1;
+        c->launches += 2;
     }
     c->packed_rank = rank;
     return GTC_OK;
@@ -391,9 +389,9 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     if (bytes < L.total) return fail(c, GTC_EINVAL, "workspace too small");
     DeviceGuard g(c->device);
     unsigned char* b = static_cast<unsigned char*>(dev_ptr);
-    // control block, chunk sums, tags (epoch 0 = never published) and the
+    // control block, group sums, tags (epoch 0 = never published) and the
     // contiguous header/offsets start at 0
-    cudaError_t e = cudaMemset(b, 0, L.chunk_sum + sizeof(unsigned) * kMaxChunks);
+    cudaError_t e = cudaMemset(b, 0, L.seg_tags[0]);
     for (int i = 0; i < L.nseg && e == cudaSuccess; ++i)
         e = cudaMemset(b + L.seg_tags[i], 0, L.seg_words[i] - L.seg_tags[i]);
     if (e == cudaSuccess) e = cudaMemset(b + L.msg_hdr, 0, L.msg_words - L.msg_hdr);
@@ -448,15 +446,12 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     p.tau = c->tau;
     p.seg = reinterpret_cast<unsigned*>(c->ws + c->L.seg_words[par]);
     p.tags = reinterpret_cast<unsigned long long*>(c->ws + c->L.seg_tags[par]);
-    p.chunk_sum = reinterpret_cast<unsigned*>(c->ws + c->L.chunk_sum);
     p.ctrl = c->ctrl;
     p.epoch = c->epoch;
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     p.num_tiles = c->num_tiles;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "encode: launch");
-    c->chunk_tiles = p.chunk_tiles;
-    c->num_chunks = p.num_chunks;
     c->launches += 1;
     c->stage = Stage::kEncoded;
     return GTC_OK;
@@ -549,8 +544,7 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
         }
         p.epoch = c->epoch;
         p.wait = c->world > 1 ? 1 : 0;
-        p.chunk_sum = reinterpret_cast<const unsigned*>(c->ws + c->L.chunk_sum);
-        p.num_chunks = c->num_chunks;
+        p.own_tags = reinterpret_cast<const unsigned long long*>(c->ws + c->L.seg_tags[par]);
         p.k_out = &c->ctrl->k;
     } else {
         p.segmented = 0;
@@ -682,16 +676,17 @@ gtc_status gtc_last_counts(gtc_ctx* c, int64_t* k_per_rank) {
     DeviceGuard g(c->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "last_counts: sync");
-    // sum of every rank's chunk sums of the last encode
+    // sum of every rank's tile counts of the last encode
+    const int par = seg_parity(c);
+    std::vector<unsigned long long> tags(c->num_tiles);
     for (int i = 0; i < c->world; ++i) {
-        std::vector<unsigned> cs(c->num_chunks, 0u);
         if (c->num_tiles > 0) {
-            e = cudaMemcpy(cs.data(), rank_ws(c, i) + c->L.chunk_sum, sizeof(unsigned) * c->num_chunks,
-                           cudaMemcpyDeviceToHost);
+            e = cudaMemcpy(tags.data(), rank_ws(c, i) + c->L.seg_tags[par],
+                           sizeof(unsigned long long) * c->num_tiles, cudaMemcpyDeviceToHost);
             if (e != cudaSuccess) return cuda_fail(c, e, "last_counts: readback");
         }
         long long k = 0;
-        for (unsigned v : cs) k += v;
+        for (unsigned long long v : tags) k += (long long)(v & 0xffffffffull);
         k_per_rank[i] = k;
     }
     return GTC_OK;

@@ -61,23 +61,23 @@ struct EncodeParams {
     float tau;
     unsigned int* seg;             // [num_tiles * kTile] tile-major words
     unsigned long long* tags;      // [num_tiles] (epoch << 32) | count
-    unsigned int* chunk_sum;       // [num_chunks] words per kernel-1 chunk
     Ctrl* ctrl;
     unsigned epoch;
     int publish_sys;               // peers read the tags: release at system scope
     int num_tiles;
-    int chunk_tiles;               // tiles per kernel-1 CTA (set by launch_encode)
-    int num_chunks;                // kernel-1 grid (set by launch_encode)
+    int chunk_tiles;               // persistent variant: tiles per CTA (set by launch_encode)
+    int num_chunks;                // persistent variant: grid (set by launch_encode)
 };
 
-// Most kernel-1 CTAs (chunks) a launch may use: 148 SMs x 2, with headroom.
+// Most persistent-encode CTAs (chunks) a launch may use.
 constexpr int kMaxChunks = 1024;
+// Packing a segmented message first sums the counts of groups of kGroupTiles tiles.
+constexpr int kGroupTiles = 64;
 
 struct CompactParams {             // segmented (any rank) -> contiguous (local)
     const unsigned int* seg;
     const unsigned long long* tags;
-    const unsigned int* chunk_sum;
-    int chunk_tiles;
+    unsigned int* group_sum;       // [ceil(num_tiles / kGroupTiles)] local scratch
     int num_tiles;
     unsigned int* words;
     int* tile_off;                 // [num_tiles + 1]
@@ -103,9 +103,8 @@ struct DecodeParams {
     signed char* counts_out;       // may be null
     unsigned long long* flags;     // this rank's Ctrl::flags
     int tiles_per_cta;             // set by launch_decode_apply
-    // segmented: block 0 also totals this rank's chunk sums into *k_out
-    const unsigned int* chunk_sum;
-    int num_chunks;
+    // segmented: block 0 also totals this rank's tile counts into *k_out
+    const unsigned long long* own_tags;
     long long* k_out;
 };
 

@@ -101,5 +101,38 @@ def main():
     print(f"cuda graph: device {e0.elapsed_time(e1) / (R * G) * 1e3:.1f} us/step")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def reference_stream():
+    """Achievable HBM rate for the encode's traffic shape (read g, read r, write r)."""
+    n = synth.LSTM_AM_PARAMS
+    dev = torch.device("cuda", 0)
+    gs = [torch.randn(n, device=dev) for _ in range(3)]
+    r = torch.randn(n, device=dev)
+    s = torch.cuda.current_stream()
+    for t in range(20):
+        r.add_(gs[t % 3])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = 2000
+    e0.record(s)
+    for t in range(K):
+        r.add_(gs[t % 3])
+    e1.record(s)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / K * 1e3
+    print(f"torch r.add_(g) (12 B/param): {us:.1f} us -> {12 * n / us / 1e3:.0f} GB/s")
+    dst = torch.empty_like(r)
+    e0.record(s)
+    for t in range(K):
+        dst.copy_(gs[t % 3])
+    e1.record(s)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / K * 1e3
+    print(f"torch copy (8 B/param): {us:.1f} us -> {8 * n / us / 1e3:.0f} GB/s")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ref":
+    reference_stream()
