@@ -10,9 +10,9 @@
 // gtc_decode_apply_kernel (any number of messages):
 //   One CTA per tiles_per_cta consecutive tiles of kTile params; the grid is
 //   one wave of resident CTAs.  Per CTA:
-//   0. p2p: thread-parallel spin (acquire, system scope) on every rank's tags
-//      of the CTA's tiles until they carry this step's epoch -- the exchange
-//      is this tile-granular wait, overlapped with the other CTAs' work;
+//   0. p2p: one thread per rank acquires (system scope) that rank's ready flag
+//      for this step, raised by its last encode CTA -- the exchange is this
+//      wait plus the NVLink reads below; no collective, no host sync;
 //   1. counts c[0..span) in shared memory, int8 (|c| <= nmsg <= 64);
 //   2. ordered per-message passes over the CTA's words of each message:
 //      indices are unique within a message, so in one pass no two threads
@@ -59,20 +59,25 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-// Count of tile t of a segmented message; in p2p mode wait (acquire, system
-// scope) until the owner has published this step's tag.  Returns -1 on timeout.
-__device__ __forceinline__ int seg_count(const DecodeParams& p, int m, long long t) {
-    if (!p.wait) return (int)(__ldcg(p.tags[m] + t) & 0xffffffffull);
-    unsigned long long v = ld_acquire_sys(p.tags[m] + t);
-    if ((unsigned)(v >> 32) != p.epoch) {
-        const unsigned long long t0 = globaltimer_ns();
-        while ((unsigned)(v >> 32) != p.epoch) {
-            if (globaltimer_ns() - t0 > kPeerTimeoutNs) return -1;
-            __nanosleep(32);
-            v = ld_acquire_sys(p.tags[m] + t);
-        }
+// p2p: wait (acquire, system scope) until rank m has published this step's
+// message (its last encode CTA raised ready = step).  A peer can be at most
+// one step ahead (its next decode waits for this rank), hence >=.  False on
+// timeout.
+__device__ __forceinline__ bool wait_ready(const DecodeParams& p, int m) {
+    unsigned long long v = ld_acquire_sys(p.ready[m]);
+    if (v >= p.step) return true;
+    const unsigned long long t0 = globaltimer_ns();
+    while (v < p.step) {
+        if (globaltimer_ns() - t0 > kPeerTimeoutNs) return false;
+        __nanosleep(64);
+        v = ld_acquire_sys(p.ready[m]);
     }
-    return (int)(v & 0xffffffffull);
+    return true;
+}
+
+// Count of tile t of a segmented message (after wait_ready in p2p mode).
+__device__ __forceinline__ int seg_count(const DecodeParams& p, int m, long long t) {
+    return (int)(__ldcg(p.tags[m] + t) & 0xffffffffull);
 }
 
 // Block 0 (segmented): this rank's word count = sum of its tile counts.
@@ -122,18 +127,23 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     for (int q = tid; q < nq; q += kDecThreads) s_cnt4[q] = make_int4(0, 0, 0, 0);
     __syncthreads();
     if (SEG) {
-        // per (message, tile) counts; in p2p mode this is where the exchange waits
+        // p2p: this is where the exchange waits -- one thread per peer acquires
+        // its ready flag; the barrier extends the acquire to the whole CTA
+        if (p.wait) {
+            for (int m = tid; m < p.nmsg; m += kDecThreads)
+                if (!wait_ready(p, m)) s_abort = 1;
+            __syncthreads();
+            if (s_abort) {
+                if (tid == 0) atomicOr(p.flags, kFlagPeer);
+                return;
+            }
+        }
+        // per (message, tile) counts
         for (int idx = tid; idx < p.nmsg * nt; idx += kDecThreads) {
             const int m = idx / nt, i = idx - m * nt;
-            const int c = seg_count(p, m, t0 + i);
-            if (c < 0) s_abort = 1;
-            s_pre[m][i + 1] = c < 0 ? 0 : c;
+            s_pre[m][i + 1] = seg_count(p, m, t0 + i);
         }
         __syncthreads();
-        if (s_abort) {
-            if (tid == 0) atomicOr(p.flags, kFlagPeer);
-            return;
-        }
         for (int m = tid; m < p.nmsg; m += kDecThreads) {  // exclusive prefix over the CTA's tiles
             s_pre[m][0] = 0;
             for (int i = 1; i <= nt; ++i) s_pre[m][i] += s_pre[m][i - 1];

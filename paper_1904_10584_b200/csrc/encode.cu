@@ -104,6 +104,14 @@ __device__ __forceinline__ void set_comp(float4& v, int e, float x) {
     if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
 }
 
+// p2p: the last encode CTA of a step makes every CTA's stores (each fenced at
+// GPU scope before it counted itself done) visible at system scope and raises
+// this rank's ready flag; peers acquire it before reading over NVLink.
+__device__ __forceinline__ void publish_ready(const EncodeParams& p) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&p.ctrl->ready), "l"(p.step) : "memory");
+}
+
 template <bool HAS_G>
 struct Smem {
     float4 r[kStages][kVec4PerTile];
@@ -261,18 +269,16 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
             }
         }
     }
-    // Publish the chunk: every word of every tile is written (barrier), then
-    // one thread fences (system scope when peers read over NVLink) and stamps
-    // the tiles' tags; a reader that sees tag[t] with this epoch sees tile t.
+    // Publish the chunk's tags after all its words (barrier); p2p: count the
+    // chunk's tiles done, the last CTA raises the ready flag.
     __syncthreads();
     if (tid == 0) {
-        if (p.publish_sys) __threadfence_system();
-        for (long long t = t_begin; t < t_end; ++t) {
-            const unsigned long long v = make_tag(p.epoch, s_cnt[t - t_begin]);
-            if (p.publish_sys)
-                asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p.tags + t), "l"(v) : "memory");
-            else
-                p.tags[t] = v;
+        for (long long t = t_begin; t < t_end; ++t) p.tags[t] = make_tag(p.epoch, s_cnt[t - t_begin]);
+        if (p.publish_sys && t_end > t_begin) {
+            __threadfence();
+            const unsigned long long done =
+                atomicAdd(&p.ctrl->done, (unsigned long long)(t_end - t_begin)) + (unsigned long long)(t_end - t_begin);
+            if (done == p.done_target) publish_ready(p);
         }
     }
 }
@@ -413,12 +419,13 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
             }
         }
     }
-    if (p.publish_sys) {  // peers read this tile over NVLink: words first, then the tag
-        __syncthreads();
+    if (p.publish_sys) {  // p2p: peers read this message over NVLink once the rank is ready
+        __syncthreads();  // every word (and r) of this tile is stored
         if (tid == 0) {
-            __threadfence_system();
-            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p.tags + tile), "l"(make_tag(p.epoch, total))
-                         : "memory");
+            p.tags[tile] = make_tag(p.epoch, total);
+            __threadfence();
+            const unsigned long long done = atomicAdd(&p.ctrl->done, 1ull) + 1ull;
+            if (done == p.done_target) publish_ready(p);  // last CTA of this encode
         }
     }
 }

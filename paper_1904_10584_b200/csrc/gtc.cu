@@ -123,6 +123,7 @@ struct gtc_ctx {
     std::vector<unsigned char*> peer_ws;
     std::vector<void*> peer_alloc;  // what cudaIpcOpenMemHandle returned (to close)
     unsigned epoch = 0;             // step counter: tag stamp; parity selects the p2p buffer
+    unsigned long long encodes = 0; // encodes since bind (p2p done-counter target)
     int packed_rank = -1;           // whose message the contiguous region holds (-1: stale)
 
     long long* host_kx = nullptr;  // pinned, 2 * world
@@ -418,6 +419,7 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
         }
     }
     c->epoch = 0;
+    c->encodes = 0;
     c->bound = true;
     c->stage = Stage::kBound;
     return GTC_OK;
@@ -450,6 +452,9 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     p.epoch = c->epoch;
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     p.num_tiles = c->num_tiles;
+    c->encodes += 1;
+    p.done_target = c->encodes * (unsigned long long)c->num_tiles;
+    p.step = c->encodes;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "encode: launch");
     c->launches += 1;
@@ -543,7 +548,10 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
             p.tags[i] = reinterpret_cast<const unsigned long long*>(b + c->L.seg_tags[par]);
         }
         p.epoch = c->epoch;
+        p.step = c->encodes;
         p.wait = c->world > 1 ? 1 : 0;
+        for (int i = 0; i < c->world && p.wait; ++i)
+            p.ready[i] = &reinterpret_cast<Ctrl*>(rank_ws(c, i) + c->L.ctrl)->ready;
         p.own_tags = reinterpret_cast<const unsigned long long*>(c->ws + c->L.seg_tags[par]);
         p.k_out = &c->ctrl->k;
     } else {

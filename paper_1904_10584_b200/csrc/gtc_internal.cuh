@@ -32,6 +32,8 @@ enum : unsigned long long {
 struct alignas(256) Ctrl {
     long long k;                  // words of the last encode (set by compaction / decode)
     unsigned long long flags;     // sticky flags
+    unsigned long long done;      // p2p: encode CTAs finished since bind (monotonic)
+    unsigned long long ready;     // p2p: step (encodes since bind) of the last published message
 };
 
 // Header of a contiguous message region.
@@ -44,9 +46,11 @@ struct MsgHeader {
 // The hot path's message is SEGMENTED: encode kernel 1 compacts the words of
 // tile t (ascending index) into slot t of a tile-major buffer,
 //     words of tile t = seg[t * kTile .. t * kTile + count_t),
-// and publishes tag[t] = (epoch << 32) | count_t after them (release at system
-// scope when peers read it over NVLink).  Decode reads exactly the words of
-// the tiles it owns, from every rank, without a global prefix scan.
+// and tag[t] = (epoch << 32) | count_t.  In p2p mode every encode CTA fences
+// (GPU scope) and counts itself done; the last one fences at system scope and
+// raises Ctrl::ready = step, which peers acquire before reading the message
+// over NVLink.  Decode reads exactly the words of the tiles it owns, from
+// every rank, without a global prefix scan.
 // The CONTIGUOUS message (words in one array + per-tile offsets + header) is
 // the wire format of the NCCL exchange and of gtc_message; gtc_compact_kernel
 // builds it from a segmented one on demand.
@@ -63,7 +67,9 @@ struct EncodeParams {
     unsigned long long* tags;      // [num_tiles] (epoch << 32) | count
     Ctrl* ctrl;
     unsigned epoch;
-    int publish_sys;               // peers read the tags: release at system scope
+    int publish_sys;               // p2p: peers read this message over NVLink
+    unsigned long long done_target;  // p2p: Ctrl::done after this encode's last tile
+    unsigned long long step;       // p2p: encodes since bind (the value raised in Ctrl::ready)
     int num_tiles;
     int chunk_tiles;               // persistent variant: tiles per CTA (set by launch_encode)
     int num_chunks;                // persistent variant: grid (set by launch_encode)
@@ -92,8 +98,10 @@ struct DecodeParams {
     const int* off[GTC_MAX_MSGS];                  // contiguous: [num_tiles + 1] tile offsets
     const unsigned int* seg[GTC_MAX_MSGS];         // segmented (peer pointers in p2p)
     const unsigned long long* tags[GTC_MAX_MSGS];  // segmented
-    unsigned epoch;                // segmented: tags of this step
-    int wait;                      // segmented: spin until a tag carries this epoch (p2p)
+    unsigned epoch;                // segmented: this step's epoch
+    unsigned long long step;       // p2p: wait until every rank's Ctrl::ready >= step
+    int wait;                      // segmented p2p: acquire every rank's ready flag first
+    const unsigned long long* ready[GTC_MAX_MSGS];  // p2p: each rank's Ctrl::ready
     int nmsg;
     long long n;
     int num_tiles;
