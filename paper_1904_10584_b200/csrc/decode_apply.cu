@@ -36,6 +36,7 @@
 #include "gtc_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace gtc {
 namespace {
@@ -420,9 +421,20 @@ cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// GTC_DECODE_GENERAL=1 routes one-message decodes through the counting
+// kernel too (for measurement).
+bool force_general() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_DECODE_GENERAL");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 template <int MODE>
 cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
-    if (p.nmsg == 1 && p.counts_out == nullptr && !p.wait) {
+    if (p.nmsg == 1 && p.counts_out == nullptr && !p.wait && !force_general()) {
         if (p.segmented) {
             const int grid = (int)std::min<long long>((p.num_tiles + 7) / 8, (long long)sm_count() * 8);
             gtc_apply_single_seg_kernel<MODE><<<grid, kSingleThreads, 0, s>>>(p);
