@@ -243,16 +243,17 @@ def run_gtc(args):
         step(t)
     torch.cuda.synchronize()
 
-    # Timed region: K steps through the one-call C entry point; every
-    # EV_EVERY-th step runs as the three separate calls with CUDA events
-    # between them (same stream), which gives the per-kernel durations.
+    # Timed region: K steps through the one-call C entry point (gtc_step: at
+    # world 1 a single fused kernel; at world > 1 encode + p2p decode).  Every
+    # EV_EVERY-th step is bracketed by CUDA events (same stream): at world 1
+    # that is the fused kernel's duration; at world > 1 those steps run as the
+    # three separate calls with events between them (per-kernel durations).
     K = args.steps
     EV_EVERY = 8
     stepf = ctx.stepper(grads, r, w, args.alpha, gtc.GTC_ACCUM_WEIGHTS, stream)
     inst = [t for t in range(K) if t % EV_EVERY == 0]
     ev = {t: [torch.cuda.Event(enable_timing=True) for _ in range(4)] for t in inst}
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kptr = ctx.local_count_tensor()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.6)
@@ -265,13 +266,20 @@ def run_gtc(args):
     for t in range(K):
         if t % EV_EVERY == 0:
             e = ev[t]
-            e[0].record(stream)
-            ctx.encode(grads[t % N_GRAD_BUFFERS], r)
-            e[1].record(stream)
-            ctx.exchange()
-            e[2].record(stream)
-            ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
-            e[3].record(stream)
+            if world == 1:
+                e[0].record(stream)
+                stepf(t)
+                e[1].record(stream)
+                e[2].record(stream)
+                e[3].record(stream)
+            else:
+                e[0].record(stream)
+                ctx.encode(grads[t % N_GRAD_BUFFERS], r)
+                e[1].record(stream)
+                ctx.exchange()
+                e[2].record(stream)
+                ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
+                e[3].record(stream)
         else:
             stepf(t)
     e_end.record(stream)
@@ -290,6 +298,23 @@ def run_gtc(args):
     ks_local = ctx.last_counts()
     k_rank = ks_local[rank] if world > 1 else ks_local[0]
 
+    # unfused breakdown (world 1; untimed by the step metric): encode kernel
+    # alone and the decode kernel alone, CUDA events on the stream
+    brk = None
+    if world == 1:
+        B = 64
+        eb = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(B)]
+        for t in range(B):
+            eb[t][0].record(stream)
+            ctx.encode(grads[t % N_GRAD_BUFFERS], r)
+            eb[t][1].record(stream)
+            ctx.exchange()
+            ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
+            eb[t][2].record(stream)
+        torch.cuda.synchronize()
+        brk = {"encode_only_ms": sum(e[0].elapsed_time(e[1]) for e in eb) / B,
+               "decode_only_ms": sum(e[1].elapsed_time(e[2]) for e in eb) / B}
+
     # density of the touched set (for the decode's algorithmic bytes), untimed
     cnt = torch.empty(n, dtype=torch.int8, device=dev)
     ctx.encode(grads[K % N_GRAD_BUFFERS], r)
@@ -304,6 +329,13 @@ def run_gtc(args):
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
     ms, enc_ms_max, exch_ms_max, dec_ms_max = stats.tolist()
     ms_per_step = ms / K
+    enc_ms_events = enc_ms
+    if world == 1:
+        # world 1: the step IS one kernel (the fused encode); its average
+        # launch duration over the timed region, launch gaps included, is the
+        # region's event time / K (the bracketing events of the sampled steps
+        # stall the stream and would overstate it)
+        enc_ms = ms_per_step
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -315,7 +347,7 @@ def run_gtc(args):
         for t in range(2):
             gdev.copy_(pinned[t % N_GRAD_BUFFERS], non_blocking=True)
             ctx.step(gdev, r, w, args.alpha)
-            k_host.copy_(kptr, non_blocking=True)
+            k_host.copy_(ctx.local_count_tensor(), non_blocking=True)
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -325,7 +357,7 @@ def run_gtc(args):
         for t in range(E):
             gdev.copy_(pinned[t % N_GRAD_BUFFERS], non_blocking=True)
             ctx.step(gdev, r, w, args.alpha)
-            k_host.copy_(kptr, non_blocking=True)
+            k_host.copy_(ctx.local_count_tensor(), non_blocking=True)
             stream.synchronize()
             _ = int(k_host[0])
         s1.record(stream)
@@ -346,15 +378,22 @@ def run_gtc(args):
         ctx.close()
         return 0
 
-    # ---- roofline of the dominant kernel (encode) and the decode
+    # ---- roofline of the dominant kernel and the decode
     peak, peak_src = measured_peaks()
     ntiles = math.ceil(n / gtc.GTC_TILE)
-    enc_bytes = 12 * n + 4 * k_rank + 4 * (ntiles + 1)
+    if world == 1:
+        # the fused step kernel: stream g, r -> r (12 B/param), words (4 k),
+        # tags (8 B/tile), target read-modify-write of the k touched elements
+        enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles + 8 * k_rank
+        kernel_name = "gtc_encode_tile_kernel (fused apply, world 1)"
+    else:
+        enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles
+        kernel_name = "gtc_encode_tile_kernel"
     enc_gbs = enc_bytes / (enc_ms * 1e-3) / 1e9
     sum_k = sum(k_all)
-    dec_bytes = 4 * sum_k + 4 * world * (ntiles + 1) + 8 * nnz_c
-    dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9 if dec_ms > 0 else None
-    step_bytes = enc_bytes + dec_bytes + (4 * (world - 1) * max(k_all) if world > 1 else 0)
+    dec_bytes = 4 * sum_k + 8 * world * ntiles + 8 * nnz_c
+    dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9 if world > 1 and dec_ms > 0 else None
+    step_bytes = enc_bytes + (dec_bytes + 4 * (world - 1) * max(k_all) if world > 1 else 0)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "encode_dram_bytes.json")
     if os.path.exists(tpath):
@@ -381,12 +420,14 @@ def run_gtc(args):
                    "exchange": ctx.exchange_mode(),
                    "l2": f"inputs larger than L2: g rotates over {N_GRAD_BUFFERS} buffers, "
                          f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},
-        "roofline": {"bound": "hbm", "kernel": "gtc_encode_kernel", "achieved": enc_gbs, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": enc_gbs, "peak": peak,
                      "unit": "GB/s", "frac": enc_gbs / peak, "traffic": traffic,
                      "alg_bytes_per_launch": enc_bytes, "ms_per_launch": enc_ms,
                      "peak_source": peak_src,
+                     "ms_per_launch_sampled_events": enc_ms_events,
                      "share_of_step": enc_ms / ms_per_step},
         "kernels": {"encode_ms": enc_ms, "exchange_ms": exch_ms, "decode_apply_ms": dec_ms,
+                    "unfused_breakdown": brk,
                     "decode_apply_GBs": dec_gbs, "decode_alg_bytes": dec_bytes, "nnz_counts": nnz_c,
                     "k_per_rank": k_all,
                     "step_alg_bytes": step_bytes,

@@ -81,22 +81,6 @@ __device__ __forceinline__ int seg_count(const DecodeParams& p, int m, long long
     return (int)(__ldcg(p.tags[m] + t) & 0xffffffffull);
 }
 
-// Block 0 (segmented): this rank's word count = sum of its tile counts.
-__device__ void total_words(const DecodeParams& p) {
-    __shared__ unsigned long long s_k[32];
-    unsigned long long k = 0;
-    for (int i = threadIdx.x; i < p.num_tiles; i += blockDim.x) k += __ldcg(p.own_tags + i) & 0xffffffffull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(kFullMask, k, o);
-    if ((threadIdx.x & 31) == 0) s_k[threadIdx.x >> 5] = k;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_k[w];
-        *p.k_out = (long long)t;
-    }
-}
-
 template <int MODE>
 __device__ __forceinline__ void apply_one(const DecodeParams& p, long long gi, int c, float t) {
     const float u = __fmul_rn((float)c, p.tau);
@@ -112,7 +96,6 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     __shared__ unsigned short s_list[kMaxTouched];  // local indices with c != 0 (< 32768)
     __shared__ int s_abort;
 
-    if (SEG && blockIdx.x == 0 && p.k_out) total_words(p);
     if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;  // nothing is applied
 
     signed char* s_cnt = reinterpret_cast<signed char*>(s_cnt4);
@@ -333,7 +316,6 @@ __device__ __forceinline__ void apply_words(const DecodeParams& p, const unsigne
 // segmented: one warp per tile
 template <int MODE>
 __global__ void __launch_bounds__(kSingleThreads) gtc_apply_single_seg_kernel(const DecodeParams p) {
-    if (blockIdx.x == 0 && p.k_out) total_words(p);
     if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long stride = (long long)gridDim.x * (kSingleThreads / 32);

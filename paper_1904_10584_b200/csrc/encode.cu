@@ -247,6 +247,8 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
             if (lane == 31) {
                 s_total = incl;
                 s_cnt[it] = incl;
+                if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);
+                if (tile == 0) *p.k_next = 0ull;
             }
         }
         __syncthreads();  // tile-local offsets known
@@ -360,6 +362,30 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
         }
     }
 
+    // world 1 fused apply (gtc_step): this rank's own quanta are the whole
+    // aggregate; load the selected targets now so the latency overlaps the
+    // residual store, the scan and the word stores below.
+    // (the first kEarly selected elements of the thread; at rho ~ 1 % a thread
+    // holds ~0.16 of its 16, the rest, if any, are loaded late)
+    constexpr int kEarly = 4;
+    int eb[kEarly];
+    float tv[kEarly];
+    unsigned late = 0u;
+    if (p.target) {
+        unsigned rem = sel;
+#pragma unroll
+        for (int q = 0; q < kEarly; ++q) {
+            eb[q] = -1;
+            if (rem) {
+                const int b = __ffs(rem) - 1;
+                rem &= rem - 1u;
+                eb[q] = b;
+                tv[q] = p.target[base + (long long)((b >> 2) * kTileThreads + tid) * 4 + (b & 3)];
+            }
+        }
+        late = rem;
+    }
+
     if (full_tile) {
         float4* r4 = reinterpret_cast<float4*>(p.r + base);
 #pragma unroll
@@ -400,6 +426,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
         if (lane == 31) {
             s_total = incl;
             if (!p.publish_sys) p.tags[tile] = make_tag(p.epoch, incl);  // read by later kernels only
+            if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);    // integer: order-free
+            if (tile == 0) *p.k_next = 0ull;
         }
     }
     __syncthreads();
@@ -417,6 +445,24 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
                     ++o;
                 }
             }
+        }
+    }
+    if (p.target && sel) {
+        // world 1 fused apply (loads issued early, see above): c = +-1 on the
+        // selected elements, fl(+-1 * tau) = +-tau, target = fmaf(alpha, +-tau,
+        // target) (R8) -- identical to decode_apply.
+        auto apply = [&](int b, float t) {
+            const float q = ((neg >> b) & 1u) ? -tau : tau;
+            p.target[base + (long long)((b >> 2) * kTileThreads + tid) * 4 + (b & 3)] =
+                (p.accum_mode == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, q, t) : __fadd_rn(t, q);
+        };
+#pragma unroll
+        for (int q = 0; q < kEarly; ++q)
+            if (eb[q] >= 0) apply(eb[q], tv[q]);
+        while (late) {
+            const int b = __ffs(late) - 1;
+            late &= late - 1u;
+            apply(b, p.target[base + (long long)((b >> 2) * kTileThreads + tid) * 4 + (b & 3)]);
         }
     }
     if (p.publish_sys) {  // p2p: peers read this message over NVLink once the rank is ready
@@ -494,7 +540,6 @@ __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const Comp
         if (tile == p.num_tiles - 1) {
             const long long k = dst0 + my_cnt;
             p.tile_off[p.num_tiles] = (int)k;
-            p.ctrl->k = k;
             unsigned long long f = *reinterpret_cast<volatile unsigned long long*>(&p.ctrl->flags);
             if (k > p.capacity) {
                 atomicOr(&p.ctrl->flags, kFlagCapacity);
@@ -571,7 +616,7 @@ bool use_persistent() {
 
 template <int CMP>
 cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
-    if (use_persistent()) return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
+    if (use_persistent() && !p.target) return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
     return p.g ? launch_tile<CMP, true>(p, s) : launch_tile<CMP, false>(p, s);
 }
 

@@ -425,7 +425,8 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     return GTC_OK;
 }
 
-gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream) {
+static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream,
+                              float* fused_target, float fused_alpha, int fused_mode) {
     if (!c) return GTC_EINVAL;
     if (!c->bound) return fail(c, GTC_ESTATE, "encode: workspace not bound");
     if (c->n > 0 && !residual) return fail(c, GTC_EINVAL, "encode: residual is null");
@@ -435,7 +436,7 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     c->epoch = c->epoch == 0xffffffffu ? 1u : c->epoch + 1u;  // 0 is never a published stamp
     c->packed_rank = -1;
     if (c->num_tiles == 0) {  // n == 0: empty message
-        cudaError_t e = cudaMemsetAsync(&c->ctrl->k, 0, sizeof(long long), stream);
+        cudaError_t e = cudaMemsetAsync(&c->ctrl->k_acc[c->epoch & 1u], 0, sizeof(unsigned long long), stream);
         if (e != cudaSuccess) return cuda_fail(c, e, "encode: n == 0");
         c->stage = Stage::kEncoded;
         return GTC_OK;
@@ -449,6 +450,11 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     p.seg = reinterpret_cast<unsigned*>(c->ws + c->L.seg_words[par]);
     p.tags = reinterpret_cast<unsigned long long*>(c->ws + c->L.seg_tags[par]);
     p.ctrl = c->ctrl;
+    p.k_acc = &c->ctrl->k_acc[c->epoch & 1u];
+    p.k_next = &c->ctrl->k_acc[(c->epoch + 1u) & 1u];
+    p.target = fused_target;
+    p.alpha = fused_alpha;
+    p.accum_mode = fused_mode;
     p.epoch = c->epoch;
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     p.num_tiles = c->num_tiles;
@@ -462,12 +468,16 @@ gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream
     return GTC_OK;
 }
 
+gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream) {
+    return encode_impl(c, grad, residual, stream, nullptr, 0.f, GTC_ACCUM_WEIGHTS);
+}
+
 static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
     // 0. the wire format: this rank's message, contiguous
     gtc_status s = pack_contiguous(c, c->rank, stream);
     if (s != GTC_OK) return s;
-    // 1. (k, flags) of every rank.  Ctrl::k and Ctrl::flags are adjacent.
-    ncclResult_t r = ncclAllGather(&c->ctrl->k, c->kx_all, 2, ncclInt64, c->comm, stream);
+    // 1. (k, flags) of every rank: the packed message's header.
+    ncclResult_t r = ncclAllGather(c->ws + c->L.msg_hdr, c->kx_all, 2, ncclInt64, c->comm, stream);
     if (r != ncclSuccess) return nccl_fail(c, r, "exchange: ncclAllGather(counts)");
     cudaError_t e = cudaMemcpyAsync(c->host_kx, c->kx_all, sizeof(long long) * 2 * c->world,
                                     cudaMemcpyDeviceToHost, stream);
@@ -552,8 +562,6 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
         p.wait = c->world > 1 ? 1 : 0;
         for (int i = 0; i < c->world && p.wait; ++i)
             p.ready[i] = &reinterpret_cast<Ctrl*>(rank_ws(c, i) + c->L.ctrl)->ready;
-        p.own_tags = reinterpret_cast<const unsigned long long*>(c->ws + c->L.seg_tags[par]);
-        p.k_out = &c->ctrl->k;
     } else {
         p.segmented = 0;
         for (int i = 0; i < c->world; ++i) {
@@ -578,6 +586,21 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
 
 gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha, int mode,
                     cudaStream_t stream) {
+    if (c && c->world == 1) {
+        // world 1: the aggregate is this rank's own quanta (c = +-1 on its
+        // message), so the encode kernel applies them itself: one launch per step
+        gtc_status s = check_apply_args(c, target, mode);
+        if (s != GTC_OK) return s;
+        if (c->n > 0 && c->num_tiles > 0) {
+            s = encode_impl(c, grad, residual, stream, target, alpha, mode);
+            if (s != GTC_OK) return s;
+        } else {
+            s = gtc_encode(c, grad, residual, stream);
+            if (s != GTC_OK) return s;
+        }
+        c->stage = Stage::kBound;
+        return GTC_OK;
+    }
     gtc_status s = gtc_encode(c, grad, residual, stream);
     if (s != GTC_OK) return s;
     const gtc_status sx = gtc_exchange(c, stream);
@@ -649,7 +672,7 @@ gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const 
 gtc_status gtc_local_count(const gtc_ctx* c, const int64_t** dev_k) {
     if (!c || !dev_k) return GTC_EINVAL;
     if (!c->bound) return GTC_ESTATE;
-    *dev_k = reinterpret_cast<const int64_t*>(&c->ctrl->k);
+    *dev_k = reinterpret_cast<const int64_t*>(&c->ctrl->k_acc[c->epoch & 1u]);
     return GTC_OK;
 }
 

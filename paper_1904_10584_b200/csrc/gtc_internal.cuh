@@ -30,7 +30,7 @@ enum : unsigned long long {
 // Control block at the start of the workspace.  k and flags are adjacent so
 // one 16-byte all-gather carries both (NCCL mode).
 struct alignas(256) Ctrl {
-    long long k;                  // words of the last encode (set by compaction / decode)
+    unsigned long long k_acc[2];  // words of the encode of step parity p (accumulated per tile)
     unsigned long long flags;     // sticky flags
     unsigned long long done;      // p2p: encode CTAs finished since bind (monotonic)
     unsigned long long ready;     // p2p: step (encodes since bind) of the last published message
@@ -66,6 +66,11 @@ struct EncodeParams {
     unsigned int* seg;             // [num_tiles * kTile] tile-major words
     unsigned long long* tags;      // [num_tiles] (epoch << 32) | count
     Ctrl* ctrl;
+    unsigned long long* k_acc;     // this step's word counter (tiles add their counts)
+    unsigned long long* k_next;    // the other parity's counter, zeroed for the next step
+    float* target;                 // world 1 fused apply (gtc_step): null = no apply
+    float alpha;
+    int accum_mode;
     unsigned epoch;
     int publish_sys;               // p2p: peers read this message over NVLink
     unsigned long long done_target;  // p2p: Ctrl::done after this encode's last tile
@@ -89,7 +94,7 @@ struct CompactParams {             // segmented (any rank) -> contiguous (local)
     int* tile_off;                 // [num_tiles + 1]
     MsgHeader* hdr;
     long long capacity;
-    Ctrl* ctrl;                    // local: k and the capacity flag
+    Ctrl* ctrl;                    // local: sticky flags (capacity)
 };
 
 struct DecodeParams {
@@ -111,9 +116,6 @@ struct DecodeParams {
     signed char* counts_out;       // may be null
     unsigned long long* flags;     // this rank's Ctrl::flags
     int tiles_per_cta;             // set by launch_decode_apply
-    // segmented: block 0 also totals this rank's tile counts into *k_out
-    const unsigned long long* own_tags;
-    long long* k_out;
 };
 
 struct BoundsParams {
