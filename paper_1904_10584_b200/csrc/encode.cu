@@ -8,26 +8,30 @@
 // and the selected words are compacted, in ascending index order (R4), into
 // one contiguous message.  HBM-bound: no contraction, no tensor cores.
 //
-// Kernel 1, gtc_encode_tiles_kernel (the whole hot-path encode):
-//   - persistent, 2 CTAs x 512 threads per SM; CTA b owns a contiguous chunk
-//     of tiles (kTile = 4096 params each): no CTA ever waits for another;
-//   - thread 0 keeps kStages tiles in flight with 1-D TMA bulk copies
-//     (cp.async.bulk.shared::cluster.global.mbarrier::complete_tx) of r and g
-//     into shared memory; the CTA reads its stage with conflict-free 128-bit
-//     LDS and writes r back with 128-bit coalesced stores (L1::no_allocate);
+// gtc_encode_tile_kernel (default; the hot-path encode, and at world 1 with
+//   gtc_step the whole step):
+//   - one CTA per tile of kTile = 4096 params, 256 threads, 4 CTAs per SM;
+//     every thread issues its four 128-bit loads of r and four of g before any
+//     use (g: ld.global.nc.L1::no_allocate) and writes r back with 128-bit
+//     stores; no state shared between CTAs;
 //   - element order inside a tile is (round j, warp, lane, component) =
 //     ascending index; intra-tile ranks come from three __ballot_sync/__popc
 //     per round (a thread holds <= 4 words per round) and one 32-entry warp
 //     scan over the (round, warp) totals;
-//   - the tile's words go, compacted, to slot t of the segmented message and
-//     its tag (epoch << 32 | count) is published after them (one tile later,
-//     behind the next block barrier; release at system scope when peers read
-//     it over NVLink); the chunk's word count goes to chunk_sum[b].
-// Kernel 2, gtc_compact_kernel (on demand: NCCL exchange, gtc_message): one
-//   warp per tile turns a segmented message (this rank's, or a peer's over
-//   NVLink) into the contiguous wire format: global tile offsets (sum of
-//   earlier chunks + earlier tiles of the chunk, all loads independent) and
-//   the words copied in order.
+//   - the tile's words go, compacted, to slot t of the segmented message; its
+//     tag (epoch << 32 | count) to tags[t]; its count (integer atomicAdd) to
+//     the step's word counter;
+//   - world 1 (gtc_step): the rank's own quanta are the aggregate (c = +-1),
+//     so the kernel also applies them to the target (loads issued right after
+//     the threshold test to hide their latency);
+//   - p2p: GPU-scope fence + done counter per CTA; the last CTA fences at
+//     system scope and raises the rank's ready flag.
+// gtc_encode_tiles_kernel (GTC_ENCODE_VARIANT=persistent, kept for
+//   measurement): persistent CTAs over contiguous tile chunks fed by 1-D TMA
+//   bulk copies (cp.async.bulk + mbarrier, 3 stages) -- slower in steady state.
+// Packing (on demand: NCCL exchange, gtc_message): gtc_group_sums_kernel +
+//   gtc_compact_kernel turn a segmented message (this rank's, or a peer's over
+//   NVLink) into the contiguous wire format.
 // No atomics, no memset, no state carried between calls except the epoch.
 //
 // HBM bytes per parameter (algorithmic): 4 (read g) + 4 (read r) + 4 (write r)
