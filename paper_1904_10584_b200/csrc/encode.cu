@@ -24,8 +24,7 @@
 //   - world 1 (gtc_step): the rank's own quanta are the aggregate (c = +-1),
 //     so the kernel also applies them to the target (loads issued right after
 //     the threshold test to hide their latency);
-//   - p2p: GPU-scope fence + done counter per CTA; the last CTA fences at
-//     system scope and raises the rank's ready flag.
+//   - p2p: gtc_publish_kernel follows (system fence + the rank's ready flag).
 // gtc_encode_tiles_kernel (GTC_ENCODE_VARIANT=persistent, kept for
 //   measurement): persistent CTAs over contiguous tile chunks fed by 1-D TMA
 //   bulk copies (cp.async.bulk + mbarrier, 3 stages) -- slower in steady state.
@@ -106,14 +105,6 @@ __device__ __forceinline__ float comp(const float4& v, int e) {
 }
 __device__ __forceinline__ void set_comp(float4& v, int e, float x) {
     if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
-}
-
-// p2p: the last encode CTA of a step makes every CTA's stores (each fenced at
-// GPU scope before it counted itself done) visible at system scope and raises
-// this rank's ready flag; peers acquire it before reading over NVLink.
-__device__ __forceinline__ void publish_ready(const EncodeParams& p) {
-    __threadfence_system();
-    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&p.ctrl->ready), "l"(p.step) : "memory");
 }
 
 template <bool HAS_G>
@@ -275,17 +266,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
             }
         }
     }
-    // Publish the chunk's tags after all its words (barrier); p2p: count the
-    // chunk's tiles done, the last CTA raises the ready flag.
+    // Publish the chunk's tags after all its words (barrier).
     __syncthreads();
     if (tid == 0) {
         for (long long t = t_begin; t < t_end; ++t) p.tags[t] = make_tag(p.epoch, s_cnt[t - t_begin]);
-        if (p.publish_sys && t_end > t_begin) {
-            __threadfence();
-            const unsigned long long done =
-                atomicAdd(&p.ctrl->done, (unsigned long long)(t_end - t_begin)) + (unsigned long long)(t_end - t_begin);
-            if (done == p.done_target) publish_ready(p);
-        }
     }
 }
 
@@ -429,7 +413,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
         s_scan[lane] = incl - x;
         if (lane == 31) {
             s_total = incl;
-            if (!p.publish_sys) p.tags[tile] = make_tag(p.epoch, incl);  // read by later kernels only
+            if (!p.publish_sys) p.tags[tile] = make_tag(p.epoch, incl);
             if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);    // integer: order-free
             if (tile == 0) *p.k_next = 0ull;
         }
@@ -469,15 +453,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
             apply(b, p.target[base + (long long)((b >> 2) * kTileThreads + tid) * 4 + (b & 3)]);
         }
     }
-    if (p.publish_sys) {  // p2p: peers read this message over NVLink once the rank is ready
-        __syncthreads();  // every word (and r) of this tile is stored
-        if (tid == 0) {
-            p.tags[tile] = make_tag(p.epoch, total);
-            __threadfence();
-            const unsigned long long done = atomicAdd(&p.ctrl->done, 1ull) + 1ull;
-            if (done == p.done_target) publish_ready(p);  // last CTA of this encode
-        }
-    }
+    if (p.publish_sys && tid == 0) p.tags[tile] = make_tag(p.epoch, total);  // published by gtc_publish_kernel
 }
 
 // Kernel 2 (packing, on demand): group sums of kGroupTiles tile counts, one
@@ -629,6 +605,20 @@ cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s) {
     if (p.num_tiles == 0) return cudaSuccess;
     return cmp_mode == GTC_CMP_GE ? launch_cmp<GTC_CMP_GE>(p, s) : launch_cmp<GTC_CMP_GT>(p, s);
+}
+
+// p2p: launched right after the encode kernel on the same stream.  The kernel
+// boundary orders every encode store before this kernel; one system-scope
+// fence then makes them visible to the peers and the release store raises
+// this rank's ready flag, which peers acquire before reading over NVLink.
+__global__ void gtc_publish_kernel(Ctrl* ctrl, unsigned long long step) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&ctrl->ready), "l"(step) : "memory");
+}
+
+cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s) {
+    gtc_publish_kernel<<<1, 1, 0, s>>>(ctrl, step);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s) {

@@ -459,11 +459,15 @@ static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cu
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     p.num_tiles = c->num_tiles;
     c->encodes += 1;
-    p.done_target = c->encodes * (unsigned long long)c->num_tiles;
     p.step = c->encodes;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "encode: launch");
     c->launches += 1;
+    if (p.publish_sys) {
+        e = launch_publish(c->ctrl, p.step, stream);
+        if (e != cudaSuccess) return cuda_fail(c, e, "encode: publish");
+        c->launches += 1;
+    }
     c->stage = Stage::kEncoded;
     return GTC_OK;
 }

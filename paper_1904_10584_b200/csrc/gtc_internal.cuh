@@ -32,7 +32,6 @@ enum : unsigned long long {
 struct alignas(256) Ctrl {
     unsigned long long k_acc[2];  // words of the encode of step parity p (accumulated per tile)
     unsigned long long flags;     // sticky flags
-    unsigned long long done;      // p2p: encode CTAs finished since bind (monotonic)
     unsigned long long ready;     // p2p: step (encodes since bind) of the last published message
 };
 
@@ -46,10 +45,10 @@ struct MsgHeader {
 // The hot path's message is SEGMENTED: encode kernel 1 compacts the words of
 // tile t (ascending index) into slot t of a tile-major buffer,
 //     words of tile t = seg[t * kTile .. t * kTile + count_t),
-// and tag[t] = (epoch << 32) | count_t.  In p2p mode every encode CTA fences
-// (GPU scope) and counts itself done; the last one fences at system scope and
-// raises Ctrl::ready = step, which peers acquire before reading the message
-// over NVLink.  Decode reads exactly the words of the tiles it owns, from
+// and tag[t] = (epoch << 32) | count_t.  In p2p mode a one-thread publish
+// kernel follows the encode kernel: fence at system scope, then raise
+// Ctrl::ready = step, which peers acquire before reading the message over
+// NVLink.  Decode reads exactly the words of the tiles it owns, from
 // every rank, without a global prefix scan.
 // The CONTIGUOUS message (words in one array + per-tile offsets + header) is
 // the wire format of the NCCL exchange and of gtc_message; gtc_compact_kernel
@@ -73,7 +72,6 @@ struct EncodeParams {
     int accum_mode;
     unsigned epoch;
     int publish_sys;               // p2p: peers read this message over NVLink
-    unsigned long long done_target;  // p2p: Ctrl::done after this encode's last tile
     unsigned long long step;       // p2p: encodes since bind (the value raised in Ctrl::ready)
     int num_tiles;
     int chunk_tiles;               // persistent variant: tiles per CTA (set by launch_encode)
@@ -130,6 +128,7 @@ struct BoundsParams {
 
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
+cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
 
