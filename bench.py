@@ -136,31 +136,37 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside)}
 
 
+def n_grad_buffers(n):
+    """Gradients rotate over 3 buffers (LSTM-AM sizes: g + r > L2 every step);
+    one buffer is already 32x the L2 at 1e9 params."""
+    return N_GRAD_BUFFERS if n < 100_000_000 else 1
+
+
 def make_inputs(n, tau, rho, rank, world):
-    """Per-rank synthetic inputs (host): 3 LSTM-shaped gradients, r0 ~ U(-tau, tau), w0."""
+    """Per-rank synthetic inputs (host): LSTM-shaped gradients, r0 ~ U(-tau, tau), w0."""
     sigma = synth.sigma_for_density(rho, tau, synth.mean_abs_scale(n))
     corr = 0.5 if world > 1 else 0.0
-    grads = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, rank, corr) for t in range(N_GRAD_BUFFERS)]
+    grads = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, rank, corr) for t in range(n_grad_buffers(n))]
     r0 = synth.uniform(n, -tau, tau, synth.rank_seed(rank))
     w0 = synth.normal(n, synth.BASE_SEED, 0, 11) * np.float32(0.05)  # replicated weights
     return grads, r0, w0
 
 
 # ------------------------------------------------------------------ oracle legs
-def cpu_oracle_run(n_full, tau, rho, cmp, alpha, budget_s, world=1):
+def cpu_oracle_run(n_full, tau, rho, cmp, alpha, budget_s, world=1, inputs=None):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
     import oracle
 
     cores = 1  # oracle.step is single-threaded
     n = n_full
-    grads, r0, w0 = make_inputs(n, tau, rho, 0, 1)
-    gs = [grads[t % N_GRAD_BUFFERS] for t in range(N_GRAD_BUFFERS)]
+    grads, r0, w0 = inputs if inputs is not None else make_inputs(n, tau, rho, 0, 1)
+    gs = [grads[t % len(grads)] for t in range(len(grads))]
     rs = [r0.copy() for _ in range(world)]
     w = w0.copy()
     mode = oracle.CMP_GT if cmp == "gt" else oracle.CMP_GE
     steps, t_used = 0, 0.0
     while t_used < budget_s or steps < 1:
-        g = [gs[steps % N_GRAD_BUFFERS]] * world
+        g = [gs[steps % len(gs)]] * world
         t0 = time.perf_counter()
         oracle.step(g, rs, w, tau, mode, alpha, oracle.ACCUM_WEIGHTS)
         t_used += time.perf_counter() - t0
@@ -190,10 +196,10 @@ def run_reference(args):
     rs = [r0.copy() for _ in range(world)]
     w = w0.copy()
     for t in range(args.warmup):
-        oracle.step([grads[t % N_GRAD_BUFFERS]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
+        oracle.step([grads[t % len(grads)]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
     t0 = time.perf_counter()
     for t in range(args.steps):
-        oracle.step([grads[t % N_GRAD_BUFFERS]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
+        oracle.step([grads[t % len(grads)]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
     dt = time.perf_counter() - t0
     value = world * n * args.steps / dt
     sample = f"each step: {n} of {n_full} params x {world} simulated worker(s), oracle.step single thread"
@@ -229,13 +235,17 @@ def run_gtc(args):
     n, tau = wl["n"], args.tau
     grads_h, r0_h, w0_h = make_inputs(n, tau, args.rho, rank, world)
     grads = [torch.from_numpy(g).to(dev) for g in grads_h]
+    NB = len(grads)
     r = torch.from_numpy(r0_h).to(dev)
     w = torch.from_numpy(w0_h).to(dev)
-    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp, exchange=args.exchange)
+    # the contiguous message is only built on demand (gtc_message / NCCL mode):
+    # at 1e9 params cap it at 5 % of n to save 3 GB per rank
+    cap = 0 if n < 100_000_000 or args.exchange == "nccl" else n // 20
+    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp, exchange=args.exchange, max_words_per_rank=cap)
     stream = torch.cuda.current_stream(dev)
 
     def step(t):
-        ctx.encode(grads[t % N_GRAD_BUFFERS], r)
+        ctx.encode(grads[t % NB], r)
         ctx.exchange()
         ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
 
@@ -274,7 +284,7 @@ def run_gtc(args):
                 e[3].record(stream)
             else:
                 e[0].record(stream)
-                ctx.encode(grads[t % N_GRAD_BUFFERS], r)
+                ctx.encode(grads[t % NB], r)
                 e[1].record(stream)
                 ctx.exchange()
                 e[2].record(stream)
@@ -306,7 +316,7 @@ def run_gtc(args):
         eb = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(B)]
         for t in range(B):
             eb[t][0].record(stream)
-            ctx.encode(grads[t % N_GRAD_BUFFERS], r)
+            ctx.encode(grads[t % NB], r)
             eb[t][1].record(stream)
             ctx.exchange()
             ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
@@ -317,7 +327,7 @@ def run_gtc(args):
 
     # density of the touched set (for the decode's algorithmic bytes), untimed
     cnt = torch.empty(n, dtype=torch.int8, device=dev)
-    ctx.encode(grads[K % N_GRAD_BUFFERS], r)
+    ctx.encode(grads[K % NB], r)
     ctx.exchange()
     ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS, cnt)
     nnz_c = int(torch.count_nonzero(cnt).item())
@@ -345,7 +355,7 @@ def run_gtc(args):
         gdev = torch.empty(n, dtype=torch.float32, device=dev)
         E = args.e2e_steps
         for t in range(2):
-            gdev.copy_(pinned[t % N_GRAD_BUFFERS], non_blocking=True)
+            gdev.copy_(pinned[t % NB], non_blocking=True)
             ctx.step(gdev, r, w, args.alpha)
             k_host.copy_(ctx.local_count_tensor(), non_blocking=True)
             torch.cuda.synchronize()
@@ -355,7 +365,7 @@ def run_gtc(args):
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for t in range(E):
-            gdev.copy_(pinned[t % N_GRAD_BUFFERS], non_blocking=True)
+            gdev.copy_(pinned[t % NB], non_blocking=True)
             ctx.step(gdev, r, w, args.alpha)
             k_host.copy_(ctx.local_count_tensor(), non_blocking=True)
             stream.synchronize()
@@ -407,7 +417,8 @@ def run_gtc(args):
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_oracle_run(n, tau, args.rho, args.cmp, args.alpha, args.cpu_seconds)
+        cpu = cpu_oracle_run(n, tau, args.rho, args.cmp, args.alpha, args.cpu_seconds,
+                             inputs=(grads_h, r0_h.copy(), w0_h.copy()))
 
     value = world * n / (ms_per_step * 1e-3)
     line = {
@@ -418,7 +429,7 @@ def run_gtc(args):
                    "rho_target": args.rho, "rho_measured": k_rank / n, "cmp": args.cmp,
                    "parallelism": f"dp{world}", "apply": "ACCUM_WEIGHTS",
                    "exchange": ctx.exchange_mode(),
-                   "l2": f"inputs larger than L2: g rotates over {N_GRAD_BUFFERS} buffers, "
+                   "l2": f"inputs larger than L2: g rotates over {NB} buffer(s), "
                          f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": enc_gbs, "peak": peak,
                      "unit": "GB/s", "frac": enc_gbs / peak, "traffic": traffic,

@@ -401,3 +401,52 @@ def test_config5_1e9_params_sampled():
         oracle.apply(c, w_exp, tau, -0.5, oracle.ACCUM_WEIGHTS)
         assert np.array_equal(bits(wd[a:b]), w_exp.view(np.uint32)), a
     ctx.close()
+
+
+# ------------------------------------------------------------------ bench launch configuration
+def test_config2_fused_step_full_size():
+    """The bench's N=1 step exactly: gtc_step (one fused kernel) on the LSTM-AM
+    size, 3 steps over rotating gradients, residual + weights bit-exact."""
+    n, tau = synth.LSTM_AM_PARAMS, 8.0
+    sigma = synth.sigma_for_density(0.01, tau, synth.mean_abs_scale(n))
+    gs = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, 0) for t in range(3)]
+    r_host = synth.uniform(n, -tau, tau, synth.rank_seed(0))
+    w_host = synth.normal(n, synth.BASE_SEED, 0, 11) * np.float32(0.05)
+    ctx = gtc.GTC(n, tau)
+    gd = [to_dev(g) for g in gs]
+    rd, wd = to_dev(r_host), to_dev(w_host)
+    f = ctx.stepper(gd, rd, wd, -1e-3)
+    for t in range(3):
+        f(t)
+        oracle.step([gs[t]], [r_host], w_host, tau, oracle.CMP_GT, -1e-3, oracle.ACCUM_WEIGHTS)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(rd), r_host.view(np.uint32))
+    assert_float_parity(wd.cpu().numpy(), w_host, "weights")
+    ctx.close()
+
+
+def test_config5_fused_step_1e9_sampled():
+    """n = 1e9 through gtc_step (the bench's launch configuration): residual and
+    weights in sampled windows against the oracle on that window."""
+    n, tau = 1_000_000_000, 8.0
+    free, _ = torch.cuda.mem_get_info()
+    if free < 24 * 2**30:
+        pytest.skip("needs ~24 GB free device memory")
+    sigma = synth.sigma_for_density(0.01, tau)
+    g = synth.normal(n, synth.rank_seed(0), 0) * np.float32(sigma)
+    r0 = synth.uniform(n, -tau, tau, synth.rank_seed(0))
+    w0 = synth.normal(n, 5, 0) * np.float32(0.05)
+    ctx = gtc.GTC(n, tau, max_words_per_rank=n // 20)
+    gd, rd, wd = to_dev(g), to_dev(r0), to_dev(w0)
+    ctx.step(gd, rd, wd, -0.5)
+    assert ctx.check() == gtc.GTC_OK
+    del gd
+    rng = np.random.default_rng(1)
+    T = gtc.GTC_TILE
+    for a in [0, T - 100, n - 4099, n - 1000] + list(rng.integers(0, n - 70_000, 10)):
+        b = min(n, a + 65_536)
+        rw, ww = r0[a:b].copy(), w0[a:b].copy()
+        oracle.step([g[a:b].copy()], [rw], ww, tau, oracle.CMP_GT, -0.5, oracle.ACCUM_WEIGHTS)
+        assert np.array_equal(bits(rd[a:b]), rw.view(np.uint32)), a
+        assert np.array_equal(bits(wd[a:b]), ww.view(np.uint32)), a
+    ctx.close()
