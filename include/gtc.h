@@ -220,6 +220,13 @@ int gtc_exchange_mode(const gtc_ctx* ctx);
 /* Number of kernels libgtc launched on this context so far (NCCL's excluded). */
 int64_t gtc_kernel_launches(const gtc_ctx* ctx);
 
+/* Debug: with GTC_DECODE_TRACE=1 in the environment, the counting decode
+ * kernel stamps %globaltimer (ns) at 6 phase boundaries (start, peers ready,
+ * tag counts, per-rank counts, non-zero list, end) for its first 4096 CTAs;
+ * this copies up to max_entries stamps (CTA-major) of the last decode to
+ * host memory.  Not for production use. */
+gtc_status gtc_debug_decode_trace(uint64_t* host, int max_entries);
+
 const char* gtc_strerror(gtc_status status);
 const char* gtc_last_error_detail(const gtc_ctx* ctx);
 

@@ -62,6 +62,7 @@ _SIGS = {
     "gtc_check": (_i32, [_vp, _vp]),
     "gtc_exchange_mode": (_i32, [_vp]),
     "gtc_kernel_launches": (_i64, [_vp]),
+    "gtc_debug_decode_trace": (_i32, [_vp, _i32]),
     "gtc_strerror": (ctypes.c_char_p, [_i32]),
     "gtc_last_error_detail": (ctypes.c_char_p, [_vp]),
     "gtc_destroy": (None, [_vp]),
@@ -196,6 +197,15 @@ def gtc_check(ctx, stream: int) -> int:
 
 def gtc_kernel_launches(ctx) -> int:
     return load_library().gtc_kernel_launches(ctx)
+
+
+def gtc_debug_decode_trace(max_entries: int = 4096 * 6):
+    """Debug: phase stamps (ns) of the last counting decode (GTC_DECODE_TRACE=1)."""
+    import numpy as np
+
+    buf = np.zeros(max_entries, dtype=np.uint64)
+    _chk(load_library().gtc_debug_decode_trace(buf.ctypes.data_as(_vp), max_entries), "gtc_debug_decode_trace")
+    return buf
 
 
 def gtc_strerror(status: int) -> str:

@@ -44,9 +44,16 @@ namespace {
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kPre = 2;                 // words per thread per message preloaded
 constexpr int kPreMsgs = 8;             // messages whose first words are preloaded
-constexpr int kMaxTouched = 4096;       // non-zero counts applied through the list
+constexpr int kMaxTouched = 2048;       // non-zero counts applied through the list (else dense fallback)
 constexpr int kChunksPerThread = kDecMaxTilesPerCta * (kTile / 16) / kDecThreads;
 constexpr unsigned long long kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000;
+
+// Opt-in phase trace of the counting decode (GTC_DECODE_TRACE=1): thread 0 of
+// each of the first kTraceCtas CTAs stamps %globaltimer at kTracePhases
+// phase boundaries (start, peers ready, tags, counts, list, end).
+constexpr int kTraceCtas = 4096;
+constexpr int kTracePhases = 6;
+__device__ unsigned long long g_trace[kTraceCtas * kTracePhases];
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
     unsigned long long v;
@@ -89,13 +96,22 @@ __device__ __forceinline__ void apply_one(const DecodeParams& p, long long gi, i
 
 template <int MODE, bool SEG>
 __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const DecodeParams p) {
-    extern __shared__ int4 s_cnt4[];  // tiles_per_cta * kTile int8 counts
-    __shared__ int s_beg[GTC_MAX_MSGS];                          // contiguous: first word
-    __shared__ int s_pre[GTC_MAX_MSGS][kDecMaxTilesPerCta + 1];  // words before tile i (per message)
+    // dynamic shared memory: int8 counts [tiles_per_cta * kTile] | per message
+    // the words before each of its tiles [nmsg][tiles_per_cta + 1] | first word [nmsg]
+    extern __shared__ int4 s_cnt4[];
+    const int npre = p.tiles_per_cta + 1;
+    int* s_pre_flat = reinterpret_cast<int*>(reinterpret_cast<signed char*>(s_cnt4) + p.tiles_per_cta * kTile);
+    int* s_beg = s_pre_flat + p.nmsg * npre;
+    auto s_pre = [&](int m, int i) -> int& { return s_pre_flat[m * npre + i]; };
     __shared__ unsigned s_warp[kDecThreads / 32];
     __shared__ unsigned short s_list[kMaxTouched];  // local indices with c != 0 (< 32768)
     __shared__ int s_abort;
 
+    const bool trace = p.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas;
+    auto stamp = [&](int ph) {
+        if (trace) g_trace[blockIdx.x * kTracePhases + ph] = globaltimer_ns();
+    };
+    stamp(0);
     if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;  // nothing is applied
 
     signed char* s_cnt = reinterpret_cast<signed char*>(s_cnt4);
@@ -117,6 +133,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
             for (int m = tid; m < p.nmsg; m += kDecThreads)
                 if (!wait_ready(p, m)) s_abort = 1;
             __syncthreads();
+            stamp(1);
             if (s_abort) {
                 if (tid == 0) atomicOr(p.flags, kFlagPeer);
                 return;
@@ -125,19 +142,20 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         // per (message, tile) counts
         for (int idx = tid; idx < p.nmsg * nt; idx += kDecThreads) {
             const int m = idx / nt, i = idx - m * nt;
-            s_pre[m][i + 1] = seg_count(p, m, t0 + i);
+            s_pre(m, i + 1) = seg_count(p, m, t0 + i);
         }
         __syncthreads();
         for (int m = tid; m < p.nmsg; m += kDecThreads) {  // exclusive prefix over the CTA's tiles
-            s_pre[m][0] = 0;
-            for (int i = 1; i <= nt; ++i) s_pre[m][i] += s_pre[m][i - 1];
+            s_pre(m, 0) = 0;
+            for (int i = 1; i <= nt; ++i) s_pre(m, i) += s_pre(m, i - 1);
         }
+        stamp(2);
     } else {
         for (int m = tid; m < p.nmsg; m += kDecThreads) {
             const int b = __ldg(p.off[m] + t0);
             s_beg[m] = b;
-            s_pre[m][0] = 0;
-            s_pre[m][nt] = __ldg(p.off[m] + t0 + nt) - b;
+            s_pre(m, 0) = 0;
+            s_pre(m, nt) = __ldg(p.off[m] + t0 + nt) - b;
         }
     }
     __syncthreads();
@@ -146,8 +164,8 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     auto word_at = [&](int m, int f) -> unsigned {
         if (SEG) {
             int i = 0;
-            while (i + 1 < nt && f >= s_pre[m][i + 1]) ++i;
-            return __ldcg(p.seg[m] + (long long)(t0 + i) * kTile + (f - s_pre[m][i]));
+            while (i + 1 < nt && f >= s_pre(m, i + 1)) ++i;
+            return __ldcg(p.seg[m] + (long long)(t0 + i) * kTile + (f - s_pre(m, i)));
         }
         return __ldg(p.words[m] + s_beg[m] + f);
     };
@@ -161,7 +179,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
             pre[m][u] = 0u;
             if (m < p.nmsg) {
                 const int f = u * kDecThreads + tid;
-                if (f < s_pre[m][nt]) pre[m][u] = word_at(m, f);
+                if (f < s_pre(m, nt)) pre[m][u] = word_at(m, f);
             }
         }
     }
@@ -170,7 +188,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
 #pragma unroll
     for (int m = 0; m < kPreMsgs; ++m) {
         if (m >= p.nmsg) break;
-        const int len = s_pre[m][nt];
+        const int len = s_pre(m, nt);
 #pragma unroll
         for (int u = 0; u < kPre; ++u) {
             if (u * kDecThreads + tid < len) {
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         __syncthreads();
     }
     for (int m = kPreMsgs; m < p.nmsg; ++m) {
-        const int len = s_pre[m][nt];
+        const int len = s_pre(m, nt);
         for (int f = tid; f < len; f += kDecThreads) {
             const unsigned word = word_at(m, f);
             const int local = (int)((word >> 1) - (unsigned)base);
@@ -196,6 +214,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         __syncthreads();
     }
 
+    stamp(3);
     // optional dense counts dump (tests / parity)
     if (p.counts_out) {
         for (int q = tid; q < nq; q += kDecThreads) {
@@ -246,6 +265,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         wbase += (w < warp) ? v : 0u;
         total += v;
     }
+    stamp(4);
     if (total <= (unsigned)kMaxTouched) {
         unsigned pos = wbase + incl - my;
 #pragma unroll
@@ -279,6 +299,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
             }
         }
     }
+    stamp(5);
 }
 
 // One message (world == 1, or one simulated worker): indices are unique, so
@@ -382,24 +403,39 @@ int sm_count() {
 template <int MODE, bool SEG>
 cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
     auto kern = gtc_decode_apply_kernel<MODE, SEG>;
-    static int resident[kDecMaxTilesPerCta + 1] = {0};
+    static int resident[GTC_MAX_MSGS + 1][kDecMaxTilesPerCta + 1] = {{0}};
+    auto dyn_smem = [&](int tpc) {
+        return (size_t)tpc * kTile + sizeof(int) * (size_t)p_in.nmsg * (tpc + 2);
+    };
+    static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kDecMaxTilesPerCta * kTile + sizeof(int) * GTC_MAX_MSGS *
+                                                   (kDecMaxTilesPerCta + 2));
+    if (attr != cudaSuccess) return attr;
     DecodeParams p = p_in;
     const int sms = sm_count();
     // smallest tiles_per_cta whose grid fits in one wave of resident CTAs
+    // (GTC_DECODE_TPC overrides, for measurement)
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = std::getenv("GTC_DECODE_TPC");
+        forced = e ? std::atoi(e) : 0;
+    }
     int tpc = 1;
     for (; tpc <= kDecMaxTilesPerCta; ++tpc) {
-        if (resident[tpc] == 0) {
+        int& res = resident[p.nmsg][tpc];
+        if (res == 0) {
             int r = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kDecThreads, (size_t)tpc * kTile) != cudaSuccess)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kDecThreads, dyn_smem(tpc)) != cudaSuccess)
                 r = 1;
-            resident[tpc] = r < 1 ? 1 : r;
+            res = r < 1 ? 1 : r;
         }
-        if ((long long)(p.num_tiles + tpc - 1) / tpc <= (long long)resident[tpc] * sms) break;
+        if ((long long)(p.num_tiles + tpc - 1) / tpc <= (long long)res * sms) break;
     }
     if (tpc > kDecMaxTilesPerCta) tpc = kDecMaxTilesPerCta;
+    if (forced > 0) tpc = forced < kDecMaxTilesPerCta ? forced : kDecMaxTilesPerCta;
     p.tiles_per_cta = tpc;
     const int grid = (p.num_tiles + tpc - 1) / tpc;
-    kern<<<grid, kDecThreads, (size_t)tpc * kTile, s>>>(p);
+    kern<<<grid, kDecThreads, dyn_smem(tpc), s>>>(p);
     return cudaGetLastError();
 }
 
@@ -433,6 +469,20 @@ cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s) {
     if (p.num_tiles == 0) return cudaSuccess;
     return accum_mode == GTC_ACCUM_UPDATE ? launch_mode<GTC_ACCUM_UPDATE>(p, s) : launch_mode<GTC_ACCUM_WEIGHTS>(p, s);
+}
+
+cudaError_t read_decode_trace(unsigned long long* host, int max_entries) {
+    const int n = max_entries < kTraceCtas * kTracePhases ? max_entries : kTraceCtas * kTracePhases;
+    return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n);
+}
+
+bool decode_trace_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_DECODE_TRACE");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s) {

@@ -581,6 +581,7 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     p.target = target;
     p.counts_out = reinterpret_cast<signed char*>(counts_out);
     p.flags = &c->ctrl->flags;
+    p.trace = decode_trace_enabled() ? 1 : 0;
     cudaError_t e = launch_decode_apply(p, mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "decode_apply: launch");
     if (c->num_tiles > 0) c->launches += 1;
@@ -775,6 +776,12 @@ int gtc_exchange_mode(const gtc_ctx* c) {
 }
 
 int64_t gtc_kernel_launches(const gtc_ctx* c) { return c ? c->launches : 0; }
+
+gtc_status gtc_debug_decode_trace(uint64_t* host, int max_entries) {
+    if (!host || max_entries < 0) return GTC_EINVAL;
+    return read_decode_trace(reinterpret_cast<unsigned long long*>(host), max_entries) == cudaSuccess ? GTC_OK
+                                                                                                    : GTC_ECUDA;
+}
 
 void gtc_destroy(gtc_ctx* c) {
     if (!c) return;

@@ -114,6 +114,7 @@ struct DecodeParams {
     signed char* counts_out;       // may be null
     unsigned long long* flags;     // this rank's Ctrl::flags
     int tiles_per_cta;             // set by launch_decode_apply
+    int trace;                     // GTC_DECODE_TRACE=1: stamp phase times (debug)
 };
 
 struct BoundsParams {
@@ -131,5 +132,7 @@ cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
 cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
+cudaError_t read_decode_trace(unsigned long long* host, int max_entries);
+bool decode_trace_enabled();
 
 }  // namespace gtc

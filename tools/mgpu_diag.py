@@ -58,5 +58,58 @@ def main():
     dist.destroy_process_group()
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and os.environ.get("DIAG_TRACE") != "1":
     main()
+
+
+def trace_report(tag, tr, ncta):
+    import numpy as np
+
+    t = tr[: ncta * 6].reshape(ncta, 6).astype(np.int64)
+    t = t[t[:, 0] > 0]
+    base = t[:, 0].min()
+    rel = (t - base) / 1e3
+    ph = np.diff(t, axis=1) / 1e3
+    names = ["wait", "tags", "counts", "list", "apply"]
+    s = ", ".join(f"{nm} med {np.median(ph[:, i]):.1f} p90 {np.percentile(ph[:, i], 90):.1f}" for i, nm in enumerate(names))
+    st = rel[:, 0]
+    en = rel[:, 5]
+    print(f"[{tag}] CTAs {len(t)}: start p10/p50/p90/max {np.percentile(st, 10):.1f}/{np.percentile(st, 50):.1f}/"
+          f"{np.percentile(st, 90):.1f}/{st.max():.1f} us, end p50/max {np.percentile(en, 50):.1f}/{en.max():.1f} us; "
+          f"by blockIdx: first-8 start {st[:8].round(1).tolist()}, last-8 start {st[-8:].round(1).tolist()}; {s}",
+          flush=True)
+
+
+def traced():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", device_id=dev)
+    n, tau = synth.LSTM_AM_PARAMS, 8.0
+    sigma = synth.sigma_for_density(0.01, tau, synth.mean_abs_scale(n))
+    grads = [torch.from_numpy(synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, rank, 0.5)).to(dev) for t in range(3)]
+    r = torch.from_numpy(synth.uniform(n, -tau, tau, synth.rank_seed(rank))).to(dev)
+    w = torch.zeros(n, device=dev)
+    ctx = gtc.GTC(n, tau, rank, world, dev)
+    for t in range(30):
+        ctx.step(grads[t % 3], r, w, -1e-3)
+    torch.cuda.synchronize()
+    ncta = 4096
+    tr = gtc.gtc_debug_decode_trace()
+    if rank == 0:
+        trace_report(f"pipelined N={world}", tr, ncta)
+    ctx.encode(grads[0], r)
+    ctx.exchange()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ctx.decode_apply(w, -1e-3)
+    torch.cuda.synchronize()
+    tr = gtc.gtc_debug_decode_trace()
+    if rank == 0:
+        trace_report(f"after barrier N={world}", tr, ncta)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__" and os.environ.get("DIAG_TRACE") == "1":
+    traced()
