@@ -118,8 +118,8 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int t0 = blockIdx.x * p.tiles_per_cta;
-    const int nt = min(p.tiles_per_cta, p.num_tiles - t0);
+    const int t0 = p.tile_begin + blockIdx.x * p.tiles_per_cta;
+    const int nt = min(p.tiles_per_cta, p.tile_end - t0);
     const long long base = (long long)t0 * kTile;
     const int nq = nt * (kTile / 16);  // int4 chunks of 16 counts
 
@@ -413,6 +413,8 @@ cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
     if (attr != cudaSuccess) return attr;
     DecodeParams p = p_in;
     const int sms = sm_count();
+    const int range = p.tile_end - p.tile_begin;
+    if (range <= 0) return cudaSuccess;
     // smallest tiles_per_cta whose grid fits in one wave of resident CTAs
     // (GTC_DECODE_TPC overrides, for measurement)
     static int forced = -1;
@@ -429,12 +431,12 @@ cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
                 r = 1;
             res = r < 1 ? 1 : r;
         }
-        if ((long long)(p.num_tiles + tpc - 1) / tpc <= (long long)res * sms) break;
+        if ((long long)(range + tpc - 1) / tpc <= (long long)res * sms) break;
     }
     if (tpc > kDecMaxTilesPerCta) tpc = kDecMaxTilesPerCta;
     if (forced > 0) tpc = forced < kDecMaxTilesPerCta ? forced : kDecMaxTilesPerCta;
     p.tiles_per_cta = tpc;
-    const int grid = (p.num_tiles + tpc - 1) / tpc;
+    const int grid = (range + tpc - 1) / tpc;
     kern<<<grid, kDecThreads, dyn_smem(tpc), s>>>(p);
     return cudaGetLastError();
 }
@@ -452,7 +454,8 @@ bool force_general() {
 
 template <int MODE>
 cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
-    if (p.nmsg == 1 && p.counts_out == nullptr && !p.wait && !force_general()) {
+    if (p.nmsg == 1 && p.counts_out == nullptr && !p.wait && !force_general() && p.tile_begin == 0 &&
+        p.tile_end == p.num_tiles) {
         if (p.segmented) {
             const int grid = (int)std::min<long long>((p.num_tiles + 7) / 8, (long long)sm_count() * 8);
             gtc_apply_single_seg_kernel<MODE><<<grid, kSingleThreads, 0, s>>>(p);

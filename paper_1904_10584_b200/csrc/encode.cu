@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const long long tile = blockIdx.x;
+    const long long tile = p.tile_begin + (long long)blockIdx.x;
     const long long base = tile * kTile;
     const bool full_tile = base + kTile <= p.n;
 
@@ -579,7 +579,8 @@ template <int CMP, bool HAS_G>
 cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
     p.chunk_tiles = 1;
     p.num_chunks = p.num_tiles;
-    gtc_encode_tile_kernel<CMP, HAS_G><<<p.num_tiles, kTileThreads, 0, s>>>(p);
+    if (p.tile_end <= p.tile_begin) return cudaSuccess;
+    gtc_encode_tile_kernel<CMP, HAS_G><<<p.tile_end - p.tile_begin, kTileThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -596,7 +597,8 @@ bool use_persistent() {
 
 template <int CMP>
 cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
-    if (use_persistent() && !p.target) return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
+    if (use_persistent() && !p.target && p.tile_begin == 0 && p.tile_end == p.num_tiles)
+        return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
     return p.g ? launch_tile<CMP, true>(p, s) : launch_tile<CMP, false>(p, s);
 }
 
@@ -611,13 +613,13 @@ cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s) {
 // boundary orders every encode store before this kernel; one system-scope
 // fence then makes them visible to the peers and the release store raises
 // this rank's ready flag, which peers acquire before reading over NVLink.
-__global__ void gtc_publish_kernel(Ctrl* ctrl, unsigned long long step) {
+__global__ void gtc_publish_kernel(Ctrl* ctrl, int slot, unsigned long long step) {
     __threadfence_system();
-    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&ctrl->ready), "l"(step) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&ctrl->ready[slot]), "l"(step) : "memory");
 }
 
-cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s) {
-    gtc_publish_kernel<<<1, 1, 0, s>>>(ctrl, step);
+cudaError_t launch_publish(Ctrl* ctrl, int slot, unsigned long long step, cudaStream_t s) {
+    gtc_publish_kernel<<<1, 1, 0, s>>>(ctrl, slot, step);
     return cudaGetLastError();
 }
 

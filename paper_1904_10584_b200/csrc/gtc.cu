@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -123,7 +124,10 @@ struct gtc_ctx {
     std::vector<unsigned char*> peer_ws;
     std::vector<void*> peer_alloc;  // what cudaIpcOpenMemHandle returned (to close)
     unsigned epoch = 0;             // step counter: tag stamp; parity selects the p2p buffer
-    unsigned long long encodes = 0; // encodes since bind (p2p done-counter target)
+    unsigned long long encodes = 0; // encodes since bind (the step value of the p2p ready flags)
+    cudaStream_t side = nullptr;    // p2p gtc_step pipeline: decode chunks run here
+    cudaEvent_t ev_chunk[kMaxPipe] = {};
+    cudaEvent_t ev_join = nullptr;
     int packed_rank = -1;           // whose message the contiguous region holds (-1: stale)
 
     long long* host_kx = nullptr;  // pinned, 2 * world
@@ -425,22 +429,24 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     return GTC_OK;
 }
 
-static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream,
-                              float* fused_target, float fused_alpha, int fused_mode) {
-    if (!c) return GTC_EINVAL;
+static gtc_status check_encode_args(gtc_ctx* c, const float* grad, float* residual) {
     if (!c->bound) return fail(c, GTC_ESTATE, "encode: workspace not bound");
     if (c->n > 0 && !residual) return fail(c, GTC_EINVAL, "encode: residual is null");
     if (!aligned16(residual) || !aligned16(grad)) return fail(c, GTC_EALIGN, "encode: grad/residual alignment");
-    DeviceGuard g(c->device);
+    return GTC_OK;
+}
 
+// A new step: epoch (tag stamp, parity), step count (p2p ready value).
+static void begin_step(gtc_ctx* c) {
     c->epoch = c->epoch == 0xffffffffu ? 1u : c->epoch + 1u;  // 0 is never a published stamp
+    c->encodes += 1;
     c->packed_rank = -1;
-    if (c->num_tiles == 0) {  // n == 0: empty message
-        cudaError_t e = cudaMemsetAsync(&c->ctrl->k_acc[c->epoch & 1u], 0, sizeof(unsigned long long), stream);
-        if (e != cudaSuccess) return cuda_fail(c, e, "encode: n == 0");
-        c->stage = Stage::kEncoded;
-        return GTC_OK;
-    }
+}
+
+// Encode tiles [tb, te) of the current step on `stream`; p2p: then publish
+// them under ready slot `slot` (-1: no publish).
+static gtc_status encode_range(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream,
+                               float* fused_target, float fused_alpha, int fused_mode, int tb, int te, int slot) {
     const int par = seg_parity(c);
     EncodeParams p{};
     p.g = grad;
@@ -458,16 +464,36 @@ static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cu
     p.epoch = c->epoch;
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     p.num_tiles = c->num_tiles;
-    c->encodes += 1;
+    p.tile_begin = tb;
+    p.tile_end = te;
     p.step = c->encodes;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "encode: launch");
     c->launches += 1;
-    if (p.publish_sys) {
-        e = launch_publish(c->ctrl, p.step, stream);
+    if (slot >= 0) {
+        e = launch_publish(c->ctrl, slot, p.step, stream);
         if (e != cudaSuccess) return cuda_fail(c, e, "encode: publish");
         c->launches += 1;
     }
+    return GTC_OK;
+}
+
+static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream,
+                              float* fused_target, float fused_alpha, int fused_mode) {
+    if (!c) return GTC_EINVAL;
+    gtc_status s = check_encode_args(c, grad, residual);
+    if (s != GTC_OK) return s;
+    DeviceGuard g(c->device);
+    begin_step(c);
+    if (c->num_tiles == 0) {  // n == 0: empty message
+        cudaError_t e = cudaMemsetAsync(&c->ctrl->k_acc[c->epoch & 1u], 0, sizeof(unsigned long long), stream);
+        if (e != cudaSuccess) return cuda_fail(c, e, "encode: n == 0");
+        c->stage = Stage::kEncoded;
+        return GTC_OK;
+    }
+    s = encode_range(c, grad, residual, stream, fused_target, fused_alpha, fused_mode, 0, c->num_tiles,
+                     (c->world > 1 && c->p2p) ? 0 : -1);
+    if (s != GTC_OK) return s;
     c->stage = Stage::kEncoded;
     return GTC_OK;
 }
@@ -545,13 +571,10 @@ static gtc_status check_apply_args(gtc_ctx* c, float* target, int mode) {
     return GTC_OK;
 }
 
-gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
-                            cudaStream_t stream) {
-    if (!c) return GTC_EINVAL;
-    if (c->stage != Stage::kExchanged) return fail(c, GTC_ESTATE, "decode_apply: call gtc_exchange first");
-    gtc_status s = check_apply_args(c, target, mode);
-    if (s != GTC_OK) return s;
-    DeviceGuard g(c->device);
+// Decode + apply tiles [tb, te) of the current step on `stream` (p2p: waiting
+// on ready slot `slot` of every peer).
+static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
+                               cudaStream_t stream, int tb, int te, int slot) {
     DecodeParams p{};
     if (c->world == 1 || c->p2p) {
         const int par = seg_parity(c);
@@ -565,7 +588,7 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
         p.step = c->encodes;
         p.wait = c->world > 1 ? 1 : 0;
         for (int i = 0; i < c->world && p.wait; ++i)
-            p.ready[i] = &reinterpret_cast<Ctrl*>(rank_ws(c, i) + c->L.ctrl)->ready;
+            p.ready[i] = &reinterpret_cast<Ctrl*>(rank_ws(c, i) + c->L.ctrl)->ready[slot];
     } else {
         p.segmented = 0;
         for (int i = 0; i < c->world; ++i) {
@@ -576,6 +599,8 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     p.nmsg = c->world;
     p.n = c->n;
     p.num_tiles = c->num_tiles;
+    p.tile_begin = tb;
+    p.tile_end = te;
     p.tau = c->tau;
     p.alpha = alpha;
     p.target = target;
@@ -584,7 +609,66 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     p.trace = decode_trace_enabled() ? 1 : 0;
     cudaError_t e = launch_decode_apply(p, mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "decode_apply: launch");
-    if (c->num_tiles > 0) c->launches += 1;
+    if (te > tb) c->launches += 1;
+    return GTC_OK;
+}
+
+gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
+                            cudaStream_t stream) {
+    if (!c) return GTC_EINVAL;
+    if (c->stage != Stage::kExchanged) return fail(c, GTC_ESTATE, "decode_apply: call gtc_exchange first");
+    gtc_status s = check_apply_args(c, target, mode);
+    if (s != GTC_OK) return s;
+    DeviceGuard g(c->device);
+    s = decode_range(c, target, alpha, mode, counts_out, stream, 0, c->num_tiles, 0);
+    if (s != GTC_OK) return s;
+    c->stage = Stage::kBound;
+    return GTC_OK;
+}
+
+static int pipeline_chunks(const gtc_ctx* c) {
+    static int k = -1;
+    if (k < 0) {
+        // measured (lstm_am, 1000 steps): K=1 558 / 881 G params/s at N=2 / 4,
+        // K=2 515 / 911, K=4 398 / 720 -- off by default
+        const char* e = std::getenv("GTC_PIPELINE_CHUNKS");
+        k = e ? std::atoi(e) : 1;
+        if (k < 1) k = 1;
+        if (k > kMaxPipe) k = kMaxPipe;
+    }
+    return std::min(k, std::max(c->num_tiles, 1));
+}
+
+// p2p, world > 1: the step as K chunks of tiles.  Chunk i's encode and its
+// ready flag go on the caller's stream; chunk i's decode goes on the side
+// stream after an event on that flag, so the decode's NVLink reads and
+// scattered target updates overlap the encode of the next chunks.  The
+// caller's stream joins the side stream at the end.
+static gtc_status step_pipelined(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
+                                 int mode, cudaStream_t stream, int K) {
+    cudaError_t e = cudaSuccess;
+    if (!c->side) {
+        e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+        for (int i = 0; i < kMaxPipe && e == cudaSuccess; ++i)
+            e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(c, e, "step: pipeline setup");
+    }
+    begin_step(c);
+    const int T = c->num_tiles;
+    for (int i = 0; i < K; ++i) {
+        const int tb = (int)((long long)T * i / K), te = (int)((long long)T * (i + 1) / K);
+        gtc_status s = encode_range(c, grad, residual, stream, nullptr, 0.f, GTC_ACCUM_WEIGHTS, tb, te, i);
+        if (s != GTC_OK) return s;
+        e = cudaEventRecord(c->ev_chunk[i], stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_chunk[i], 0);
+        if (e != cudaSuccess) return cuda_fail(c, e, "step: chunk event");
+        s = decode_range(c, target, alpha, mode, nullptr, c->side, tb, te, i);
+        if (s != GTC_OK) return s;
+    }
+    e = cudaEventRecord(c->ev_join, c->side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c->ev_join, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "step: join");
     c->stage = Stage::kBound;
     return GTC_OK;
 }
@@ -605,6 +689,16 @@ gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* targe
         }
         c->stage = Stage::kBound;
         return GTC_OK;
+    }
+    if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1) {
+        const int K = pipeline_chunks(c);
+        if (K > 1) {
+            gtc_status s = check_encode_args(c, grad, residual);
+            if (s == GTC_OK) s = check_apply_args(c, target, mode);
+            if (s != GTC_OK) return s;
+            DeviceGuard g(c->device);
+            return step_pipelined(c, grad, residual, target, alpha, mode, stream, K);
+        }
     }
     gtc_status s = gtc_encode(c, grad, residual, stream);
     if (s != GTC_OK) return s;
@@ -792,6 +886,13 @@ void gtc_destroy(gtc_ctx* c) {
         // this rank is done with theirs) when the mappings go away
         int* d = reinterpret_cast<int*>(c->ws + c->L.ipc);
         if (ncclAllReduce(d, d, 1, ncclInt32, ncclSum, c->comm, 0) == ncclSuccess) cudaStreamSynchronize(0);
+    }
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        for (int i = 0; i < kMaxPipe; ++i)
+            if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
+        if (c->ev_join) cudaEventDestroy(c->ev_join);
+        cudaStreamDestroy(c->side);
     }
     for (void* p : c->peer_alloc)
         if (p) cudaIpcCloseMemHandle(p);

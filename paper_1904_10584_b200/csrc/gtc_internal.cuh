@@ -32,8 +32,10 @@ enum : unsigned long long {
 struct alignas(256) Ctrl {
     unsigned long long k_acc[2];  // words of the encode of step parity p (accumulated per tile)
     unsigned long long flags;     // sticky flags
-    unsigned long long ready;     // p2p: step (encodes since bind) of the last published message
+    unsigned long long ready[8];  // p2p: per pipeline chunk, the step (encodes since bind)
+                                  // whose message the rank has published
 };
+constexpr int kMaxPipe = 8;       // most pipeline chunks of gtc_step (p2p)
 
 // Header of a contiguous message region.
 struct MsgHeader {
@@ -74,6 +76,7 @@ struct EncodeParams {
     int publish_sys;               // p2p: peers read this message over NVLink
     unsigned long long step;       // p2p: encodes since bind (the value raised in Ctrl::ready)
     int num_tiles;
+    int tile_begin, tile_end;      // the tiles this launch encodes (pipeline chunk)
     int chunk_tiles;               // persistent variant: tiles per CTA (set by launch_encode)
     int num_chunks;                // persistent variant: grid (set by launch_encode)
 };
@@ -108,6 +111,7 @@ struct DecodeParams {
     int nmsg;
     long long n;
     int num_tiles;
+    int tile_begin, tile_end;      // the tiles this launch decodes (pipeline chunk)
     float tau;
     float alpha;
     float* target;
@@ -129,7 +133,7 @@ struct BoundsParams {
 
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
-cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s);
+cudaError_t launch_publish(Ctrl* ctrl, int slot, unsigned long long step, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
 cudaError_t read_decode_trace(unsigned long long* host, int max_entries);

@@ -64,6 +64,20 @@ def main():
         hs = [None] * world
         dist.all_gather_object(hs, h)
         assert len(set(hs)) == 1, f"replicas differ at step {t}"
+    # the one-call step (p2p: pipelined encode/decode chunks on two streams)
+    for t in range(steps, 2 * steps):
+        gs = [synth.correlated_gradient(n, 4.0, synth.BASE_SEED, t, w) for w in range(world)]
+        st = ctx.step(torch.from_numpy(gs[rank]).to(dev), rd, wd, -0.5, gtc.GTC_ACCUM_WEIGHTS)
+        assert st == gtc.GTC_OK, st
+        torch.cuda.synchronize()
+        oracle.step(gs, r_or, w_or, tau, mode, -0.5, oracle.ACCUM_WEIGHTS)
+        assert np.array_equal(rd.cpu().numpy().view(np.uint32), r_or[rank].view(np.uint32)), f"step {t}: residual"
+        wh = wd.cpu().numpy()
+        assert np.array_equal(wh.view(np.uint32), w_or.view(np.uint32)), f"step {t}: weights (gtc_step)"
+        hs = [None] * world
+        dist.all_gather_object(hs, hashlib.sha256(wh.tobytes()).hexdigest())
+        assert len(set(hs)) == 1, f"replicas differ at step {t} (gtc_step)"
+    assert ctx.check() == gtc.GTC_OK
     ctx.close()
     dist.barrier()
     dist.destroy_process_group()
