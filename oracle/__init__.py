@@ -64,6 +64,10 @@ def lib():
         L.oracle_step.argtypes = [i64, f32, i32, i32, vp, vp, vp, vp, vp, vp, f32, i32,
                                   ctypes.POINTER(i32)]
         L.oracle_step.restype = i32
+        L.oracle_bmuf_step.argtypes = [i64, i32, vp, vp, vp, f32, f32, vp]
+        L.oracle_bmuf_step.restype = i32
+        L.oracle_bmuf_zeta.argtypes = [ctypes.c_double, i32, ctypes.c_double]
+        L.oracle_bmuf_zeta.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -155,3 +159,25 @@ def step(gs, rs, target, tau: float, cmp_mode: int = CMP_GT, alpha: float = 1.0,
     if st != OK:
         raise OracleError(st, "step")
     return [words[w][: ks[w]].copy() for w in range(nw)], counts[:n].copy(), bool(nf.value)
+
+
+def bmuf_step(ws, wg, delta, eta: float, zeta: float):
+    """One BMUF step (Eqs. 1-4).  ``wg`` and ``delta`` are
+    updated in place; every worker model in ``ws`` is set to the new ``wg``."""
+    nw = len(ws)
+    for a in list(ws) + [wg, delta]:
+        _f32(a, "bmuf array")
+        if a.size != wg.size:
+            raise ValueError("size mismatch")
+    VP = ctypes.c_void_p * max(nw, 1)
+    wp = VP(*[w.ctypes.data for w in ws])
+    st = lib().oracle_bmuf_step(wg.size, nw, ctypes.cast(wp, ctypes.c_void_p), _ptr(wg), _ptr(delta),
+                                float(eta), float(zeta), ctypes.cast(wp, ctypes.c_void_p))
+    if st != OK:
+        raise OracleError(st, "bmuf_step")
+    return wg
+
+
+def bmuf_zeta(C: float, N: int, eta: float) -> float:
+    """Eq. (5): zeta = C * N * (1 - eta)."""
+    return lib().oracle_bmuf_zeta(C, N, eta)

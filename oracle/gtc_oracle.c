@@ -132,3 +132,38 @@ int oracle_step(int64_t n, float tau, int cmp_mode, int nworkers,
     if (nonfinite_out) *nonfinite_out = any_nonfinite;
     return st;
 }
+
+/* ---------------------------------------------------------------- BMUF */
+int oracle_bmuf_step(int64_t n, int nworkers, const float* const* w, float* wg, float* delta,
+                     float eta, float zeta, float* const* w_out)
+{
+    if (n < 0) return ORACLE_EDIM;
+    if (nworkers < 1) return ORACLE_EINVAL;
+    for (int64_t j = 0; j < n; ++j) {
+        /* Eq. (1): model average, worker-rank order, double accumulator */
+        double acc = 0.0;
+        for (int i = 0; i < nworkers; ++i) acc = acc + (double)w[i][j];
+        float wbar = (float)(acc / (double)nworkers);
+        /* Eq. (2) */
+        float g = wbar - wg[j];
+        /* Eq. (3) */
+        float d = eta * delta[j];
+        float zg = zeta * g;
+        d = d + zg;
+        delta[j] = d;
+        /* Eq. (4), Nesterov block momentum */
+        float x = wg[j] + d;
+        float look = eta * d;
+        x = x + look;
+        wg[j] = x;
+    }
+    /* every worker restarts from the new global model */
+    for (int i = 0; i < nworkers; ++i)
+        for (int64_t j = 0; j < n; ++j) w_out[i][j] = wg[j];
+    return ORACLE_OK;
+}
+
+double oracle_bmuf_zeta(double C, int N, double eta)
+{
+    return C * (double)N * (1.0 - eta);
+}

@@ -91,6 +91,24 @@ int oracle_step(int64_t n, float tau, int cmp_mode, int nworkers,
                 int32_t* counts, float* target, float alpha, int accum_mode,
                 int* nonfinite_out);
 
+/* ---------------------------------------------------------------- BMUF
+ * Blockwise Model Update Filtering with Nesterov block momentum, the paper's
+ * other trainer: PAPER.md:224-244 (Sec. VI-B), Eqs. (1)-(5).  One BMUF step
+ * ("the global model is updated using the following procedure"), element by
+ * element:
+ *   (1) Wbar = (1/N) sum_{i=1..N} W^i        (readings B3: sum in worker-rank
+ *       order in double, one division by N, one rounding to float)
+ *   (2) G     = fl(Wbar - Wg)
+ *   (3) Delta = fl(fl(eta * Delta) + fl(zeta * G))
+ *   (4) Wg    = fl(fl(Wg + Delta) + fl(eta * Delta))   (NBM, eta_{t+1} = eta: B1)
+ * and every worker restarts the next block from Wg (B2, "the initial
+ * global model (W_g) is broadcasted to all workers").  w_out may alias w. */
+int oracle_bmuf_step(int64_t n, int nworkers, const float* const* w, float* wg, float* delta,
+                     float eta, float zeta, float* const* w_out);
+
+/* Eq. (5): zeta / (N (1 - eta)) = C  =>  zeta = C * N * (1 - eta), in double. */
+double oracle_bmuf_zeta(double C, int N, double eta);
+
 #ifdef __cplusplus
 }
 #endif
