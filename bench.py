@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["gtc", "reference"], default="gtc")
+    ap.add_argument("--algo", choices=["gtc", "bmuf"], default="gtc",
+                    help="gtc: the GTC step (headline); bmuf: the paper's BMUF-NBM sync step (Eqs. 1-4)")
+    ap.add_argument("--bmuf-eta", type=float, default=None, help="block momentum (default 1 - 1/N)")
+    ap.add_argument("--bmuf-C", type=float, default=1.0, help="Eq. (5) constant C")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="lstm_am")
     ap.add_argument("--rho", type=float, default=0.01, help="target per-rank update density")
     ap.add_argument("--tau", type=float, default=8.0, help="gradient threshold (PAPER.md:249 uses 8)")
@@ -458,10 +462,87 @@ def run_gtc(args):
     return 0
 
 
+def run_bmuf(args):
+    """The paper's other trainer: one BMUF-NBM sync step =
+    reduce-scatter of the local models + fused Eqs. (1)-(4) on the rank's shard
+    + all-gather of Wg, timed over K steps; it runs once per block of 100
+    mini-batches (PAPER.md:249)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1904_10584_b200 as gtc
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = WORKLOADS[args.workload]["n"]
+    eta = args.bmuf_eta if args.bmuf_eta is not None else 1.0 - 1.0 / max(world, 2)
+    zeta = gtc.bmuf_zeta(args.bmuf_C, world, eta)
+    w0 = torch.from_numpy(synth.normal(n, synth.BASE_SEED, 0, 11)).to(dev)
+    b = gtc.BMUF(n, eta, zeta, rank, world, dev, w_init=w0)
+    w = b.local_buffer()
+    w[:n].copy_(w0)
+    w[:n].add_(torch.from_numpy(synth.normal(n, synth.rank_seed(rank), 1) * np.float32(1e-3)).to(dev))
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, args.warmup)):
+        b.sync(w)
+    torch.cuda.synchronize()
+    K = args.steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.6)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark()
+    e0.record(stream)
+    for _ in range(K):
+        b.sync(w)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.mark()
+    time.sleep(0.3)
+    clocks.stop()
+    ms = torch.tensor([e0.elapsed_time(e1) / K], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = ms.item()
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        hbm_bytes = 24 * b.shard  # fused kernel: read sum, Wg, Delta; write Wg, Delta, local shard
+        nvl = 2 * (world - 1) * 4 * b.shard  # reduce-scatter + all-gather bytes in and out per rank
+        line = {
+            "metric": "params/sec BMUF-NBM sync step (Eqs. 1-4)", "value": world * n / (ms * 1e-3),
+            "unit": "params/s", "n_gpus": world, "steps": K, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "algo": "bmuf",
+            "config": {"workload": args.workload, "n_params": n, "eta": eta, "zeta": zeta, "C": args.bmuf_C,
+                       "shard": b.shard, "design": "in-place NCCL reduce-scatter -> fused Eqs. (1)-(4) on the "
+                                                   "rank's shard -> in-place NCCL all-gather"},
+            "bytes_per_step": {"hbm_kernel": hbm_bytes, "nvlink_per_rank": nvl},
+            "achieved_GBs_if_hbm_only": (hbm_bytes + (2 * 4 * b.shard * (world - 1) if world > 1 else 0))
+            / (ms * 1e-3) / 1e9, "peak": peak, "peak_source": peak_src,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    b.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.algo == "bmuf":
+        return run_bmuf(args)
     return run_gtc(args)
 
 

@@ -66,6 +66,14 @@ _SIGS = {
     "gtc_strerror": (ctypes.c_char_p, [_i32]),
     "gtc_last_error_detail": (ctypes.c_char_p, [_vp]),
     "gtc_destroy": (None, [_vp]),
+    # include/bmuf.h
+    "bmuf_init": (_i32, [ctypes.POINTER(_vp), _i64, _i32, _i32, _vp, _i32]),
+    "bmuf_shard_len": (_i64, [_vp]),
+    "bmuf_padded_len": (_i64, [_vp]),
+    "bmuf_sync": (_i32, [_vp, _vp, _vp, _vp, _f32, _f32, _vp]),
+    "bmuf_sync_sim": (_i32, [_vp, _vp, _i32, _vp, _vp, _f32, _f32, _vp]),
+    "bmuf_zeta": (ctypes.c_double, [ctypes.c_double, _i32, ctypes.c_double]),
+    "bmuf_destroy": (None, [_vp]),
 }
 
 _lib = None
@@ -391,6 +399,92 @@ class GTC:
     def close(self):
         if getattr(self, "ctx", None) is not None:
             gtc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------- BMUF (include/bmuf.h)
+def bmuf_init(n: int, rank: int = 0, world: int = 1, unique_id: bytes | None = None, cuda_device: int = 0):
+    ctx = _vp()
+    uid = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None
+    _chk(load_library().bmuf_init(ctypes.byref(ctx), n, rank, world, uid, cuda_device), "bmuf_init")
+    return ctx
+
+
+def bmuf_shard_len(ctx) -> int:
+    return load_library().bmuf_shard_len(ctx)
+
+
+def bmuf_padded_len(ctx) -> int:
+    return load_library().bmuf_padded_len(ctx)
+
+
+def bmuf_sync(ctx, w_local_ptr: int, wg_shard_ptr: int, delta_shard_ptr: int, eta: float, zeta: float,
+              stream: int):
+    _chk(load_library().bmuf_sync(ctx, w_local_ptr, wg_shard_ptr, delta_shard_ptr, eta, zeta, stream), "bmuf_sync")
+
+
+def bmuf_sync_sim(ctx, w_ptrs, wg_ptr: int, delta_ptr: int, eta: float, zeta: float, stream: int):
+    P = (_vp * max(len(w_ptrs), 1))(*w_ptrs)
+    _chk(load_library().bmuf_sync_sim(ctx, P, len(w_ptrs), wg_ptr, delta_ptr, eta, zeta, stream), "bmuf_sync_sim")
+
+
+def bmuf_zeta(C: float, N: int, eta: float) -> float:
+    """Eq. (5): zeta = C * N * (1 - eta)."""
+    return load_library().bmuf_zeta(C, N, eta)
+
+
+def bmuf_destroy(ctx):
+    load_library().bmuf_destroy(ctx)
+
+
+class BMUF:
+    """One rank's BMUF-NBM synchroniser.  Holds this rank's
+    shard of the global model Wg and of the block momentum Delta (torch-owned);
+    ``sync(w_local)`` runs Eqs. (1)-(4) and leaves Wg(t) in ``w_local``."""
+
+    def __init__(self, n_params: int, eta: float, zeta: float, rank: int = 0, world: int = 1, device=None,
+                 group=None, w_init=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("BMUF needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.n, self.rank, self.world = int(n_params), int(rank), int(world)
+        self.eta, self.zeta = float(eta), float(zeta)
+        uid = broadcast_unique_id(rank, group) if world > 1 else None
+        with torch.cuda.device(self.device):
+            self.ctx = bmuf_init(self.n, rank, world, uid, self.device.index)
+        self.shard = bmuf_shard_len(self.ctx)
+        self.padded = bmuf_padded_len(self.ctx)
+        self.wg = torch.zeros(self.shard, dtype=torch.float32, device=self.device)
+        self.delta = torch.zeros(self.shard, dtype=torch.float32, device=self.device)
+        if w_init is not None:  # Wg(0): this rank's shard of the initial model
+            lo = self.rank * self.shard
+            hi = min(self.n, lo + self.shard)
+            if hi > lo:
+                self.wg[: hi - lo].copy_(w_init.reshape(-1)[lo:hi])
+
+    def local_buffer(self):
+        """A zero-padded float[padded_len] buffer for the local model."""
+        import torch
+
+        return torch.zeros(self.padded, dtype=torch.float32, device=self.device)
+
+    def sync(self, w_local, stream=None):
+        if w_local.numel() != self.padded:
+            raise ValueError("w_local must have bmuf_padded_len elements")
+        bmuf_sync(self.ctx, _ptr(w_local, "w_local"), _ptr(self.wg, "wg"), _ptr(self.delta, "delta"),
+                  self.eta, self.zeta, _stream(stream, self.device))
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            bmuf_destroy(self.ctx)
             self.ctx = None
 
     def __del__(self):

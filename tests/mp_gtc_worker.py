@@ -85,5 +85,64 @@ def main():
         print(f"MULTIGPU OK world={world} n={n} steps={steps} cmp={cmp} exchange={exchange}")
 
 
+
+
+
+def bmuf_main():
+    """One rank of the multi-GPU BMUF check (GTC_MODE=bmuf)."""
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    n = int(os.environ.get("GTC_N", 1_000_003))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    eta = 1.0 - 1.0 / world
+    zeta = 1.0  # Eq. (5) with C = 1
+    w0 = synth.normal(n, 5)
+    b = gtc.BMUF(n, eta, zeta, rank, world, dev, w_init=torch.from_numpy(w0).to(dev))
+    wg_h, d_h = w0.copy(), np.zeros(n, np.float32)
+    w = b.local_buffer()
+    eps = np.float64(2.0 ** -24)
+    for t in range(4):
+        ws_h = [(wg_h + synth.normal(n, 20 + i, t) * np.float32(0.01)).astype(np.float32) for i in range(world)]
+        w[:n].copy_(torch.from_numpy(ws_h[rank]))
+        b.sync(w)
+        torch.cuda.synchronize()
+        got = w[:n].cpu().numpy()
+        wg_prev = wg_h.astype(np.float64)
+        d_prev = d_h.astype(np.float64)
+        mean_abs = np.mean(np.abs(np.stack(ws_h).astype(np.float64)), axis=0)
+        oracle.bmuf_step([x.copy() for x in ws_h], wg_h, d_h, eta, zeta)
+        # Error bound from every rounding of Eqs. (1)-(4), with NCCL summing in
+        # its own order: |dWbar| <= (N-1) eps mean|W| + eps |Wbar| (sum, division);
+        # G, Delta and Wg add one relative eps per operation on their operands;
+        # the mean's error reaches Wg through zeta and (1 + eta).
+        G = np.abs(np.mean(np.stack(ws_h).astype(np.float64), axis=0) - wg_prev)
+        d_new = np.abs(d_h.astype(np.float64))
+        e_wbar = (world - 1) * eps * mean_abs + eps * (mean_abs + G)
+        e_d = zeta * (e_wbar + eps * G) + 2 * eps * (eta * np.abs(d_prev) + zeta * G) + eps * d_new
+        tol = (1 + eta) * e_d + 3 * eps * (np.abs(wg_prev) + (1 + eta) * d_new) \
+            + 2 * np.spacing(np.abs(wg_h)).astype(np.float64)
+        err = np.abs(got.astype(np.float64) - wg_h.astype(np.float64))
+        bad = np.argmax(err - tol)
+        assert np.all(err <= tol), f"rank {rank} step {t}: err {err[bad]} vs tol {tol[bad]} at {bad}"
+        wg_h = got.copy()  # continue from the device state (each step checked on its own)
+        lo = rank * b.shard
+        hi = min(n, lo + b.shard)
+        d_dev = b.delta[: hi - lo].cpu().numpy()
+        d_h[lo:hi] = d_dev  # likewise for Delta
+        hs = [None] * world
+        dist.all_gather_object(hs, hashlib.sha256(got.tobytes()).hexdigest())
+        assert len(set(hs)) == 1, f"ranks disagree on Wg at step {t}"
+    b.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"BMUF OK world={world} n={n}")
+
+
 if __name__ == "__main__":
-    main()
+    if os.environ.get("GTC_MODE") == "bmuf":
+        bmuf_main()
+    else:
+        main()

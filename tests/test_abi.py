@@ -7,18 +7,20 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "gtc.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("gtc.h", "bmuf.h")]
 
 
 def declared_functions():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(gtc_[a-z_]+)\s*\(", src)))
+    names = set()
+    for h in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names |= set(re.findall(r"\b((?:gtc|bmuf)_[a-z_]+)\s*\(", src))
+    return sorted(names)
 
 
 def test_header_declares_the_boundary():
     fns = declared_functions()
-    for name in ("gtc_init", "gtc_encode", "gtc_exchange", "gtc_decode_apply", "gtc_destroy"):
+    for name in ("gtc_init", "gtc_encode", "gtc_exchange", "gtc_decode_apply", "gtc_destroy", "bmuf_sync"):
         assert name in fns
 
 
