@@ -747,6 +747,8 @@ gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const 
     p.nmsg = nmsg;
     p.n = c->n;
     p.num_tiles = c->num_tiles;
+    p.tile_begin = 0;
+    p.tile_end = c->num_tiles;
     p.tau = c->tau;
     p.alpha = alpha;
     p.target = target;
