@@ -296,10 +296,15 @@ __device__ __forceinline__ float4 ld_v4(const float4* p) {
     return v;
 }
 
-template <int CMP, bool HAS_G>
-__global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const EncodeParams p) {
+// TMA = true: the tile's r (and g) arrive by two 16 KB 1-D bulk copies into
+// shared memory (one mbarrier), so the loads in flight do not occupy
+// registers and more CTAs fit per SM (GTC_ENCODE_VARIANT=tma).
+template <int CMP, bool HAS_G, bool TMA>
+__global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_kernel(const EncodeParams p) {
     __shared__ unsigned s_scan[kTileVec * kTileWarps];
     __shared__ unsigned s_total;
+    extern __shared__ __align__(128) float4 s_tile[];  // TMA: [r | g] of the tile
+    __shared__ __align__(8) unsigned long long s_bar;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -310,7 +315,22 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const 
 
     float4 rv[kTileVec];
     float4 gv[kTileVec];
-    if (full_tile) {
+    if (full_tile && TMA) {
+        if (tid == 0) {
+            mbar_init(&s_bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(&s_bar, HAS_G ? 2u * kTileBytes : (unsigned)kTileBytes);
+            tma_load_1d(s_tile, p.r + base, kTileBytes, &s_bar);
+            if (HAS_G) tma_load_1d(s_tile + kVec4PerTile, p.g + base, kTileBytes, &s_bar);
+        }
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        mbar_wait(&s_bar, 0u);
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+            rv[j] = s_tile[j * kTileThreads + tid];
+            if (HAS_G) gv[j] = s_tile[kVec4PerTile + j * kTileThreads + tid];
+        }
+    } else if (full_tile) {
         const float4* r4 = reinterpret_cast<const float4*>(p.r + base);
 #pragma unroll
         for (int j = 0; j < kTileVec; ++j) rv[j] = ld_v4(r4 + j * kTileThreads + tid);
@@ -575,24 +595,34 @@ cudaError_t launch_tiles(EncodeParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Encode variant: one tile per CTA with register loads (default, 0), the
+// same with a TMA bulk copy into shared memory (GTC_ENCODE_VARIANT=tma, 2), or
+// the persistent TMA pipeline (GTC_ENCODE_VARIANT=persistent, 1); the last
+// two are kept for measurement.
+int encode_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_ENCODE_VARIANT");
+        v = 0;
+        if (e && std::strcmp(e, "persistent") == 0) v = 1;
+        if (e && std::strcmp(e, "tma") == 0) v = 2;
+    }
+    return v;
+}
+bool use_persistent() { return encode_variant() == 1; }
+
 template <int CMP, bool HAS_G>
 cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
     p.chunk_tiles = 1;
     p.num_chunks = p.num_tiles;
     if (p.tile_end <= p.tile_begin) return cudaSuccess;
-    gtc_encode_tile_kernel<CMP, HAS_G><<<p.tile_end - p.tile_begin, kTileThreads, 0, s>>>(p);
-    return cudaGetLastError();
-}
-
-// Encode variant: one tile per CTA (default) or the persistent TMA pipeline
-// (GTC_ENCODE_VARIANT=persistent, kept for measurement).
-bool use_persistent() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("GTC_ENCODE_VARIANT");
-        v = (e && std::strcmp(e, "persistent") == 0) ? 1 : 0;
+    if (encode_variant() == 2) {
+        const size_t smem = (HAS_G ? 2 : 1) * (size_t)kTileBytes;
+        gtc_encode_tile_kernel<CMP, HAS_G, true><<<p.tile_end - p.tile_begin, kTileThreads, smem, s>>>(p);
+    } else {
+        gtc_encode_tile_kernel<CMP, HAS_G, false><<<p.tile_end - p.tile_begin, kTileThreads, 0, s>>>(p);
     }
-    return v == 1;
+    return cudaGetLastError();
 }
 
 template <int CMP>
