@@ -112,6 +112,12 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         if (trace) g_trace[blockIdx.x * kTracePhases + ph] = globaltimer_ns();
     };
     stamp(0);
+    if (p.publish && blockIdx.x == 0 && threadIdx.x == 0) {
+        // p2p: every store of this rank's encode precedes this kernel (stream
+        // order); make them visible at system scope, then tell the peers
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p.publish), "l"(p.step) : "memory");
+    }
     if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;  // nothing is applied
 
     signed char* s_cnt = reinterpret_cast<signed char*>(s_cnt4);

@@ -491,8 +491,8 @@ static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cu
         c->stage = Stage::kEncoded;
         return GTC_OK;
     }
-    s = encode_range(c, grad, residual, stream, fused_target, fused_alpha, fused_mode, 0, c->num_tiles,
-                     (c->world > 1 && c->p2p) ? 0 : -1);
+    // p2p: the decode kernel raises ready[0] when it starts (no publish launch)
+    s = encode_range(c, grad, residual, stream, fused_target, fused_alpha, fused_mode, 0, c->num_tiles, -1);
     if (s != GTC_OK) return s;
     c->stage = Stage::kEncoded;
     return GTC_OK;
@@ -574,7 +574,7 @@ static gtc_status check_apply_args(gtc_ctx* c, float* target, int mode) {
 // Decode + apply tiles [tb, te) of the current step on `stream` (p2p: waiting
 // on ready slot `slot` of every peer).
 static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
-                               cudaStream_t stream, int tb, int te, int slot) {
+                               cudaStream_t stream, int tb, int te, int slot, bool publish) {
     DecodeParams p{};
     if (c->world == 1 || c->p2p) {
         const int par = seg_parity(c);
@@ -589,6 +589,7 @@ static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode,
         p.wait = c->world > 1 ? 1 : 0;
         for (int i = 0; i < c->world && p.wait; ++i)
             p.ready[i] = &reinterpret_cast<Ctrl*>(rank_ws(c, i) + c->L.ctrl)->ready[slot];
+        if (p.wait && publish) p.publish = &c->ctrl->ready[slot];
     } else {
         p.segmented = 0;
         for (int i = 0; i < c->world; ++i) {
@@ -620,7 +621,7 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     gtc_status s = check_apply_args(c, target, mode);
     if (s != GTC_OK) return s;
     DeviceGuard g(c->device);
-    s = decode_range(c, target, alpha, mode, counts_out, stream, 0, c->num_tiles, 0);
+    s = decode_range(c, target, alpha, mode, counts_out, stream, 0, c->num_tiles, 0, true);
     if (s != GTC_OK) return s;
     c->stage = Stage::kBound;
     return GTC_OK;
@@ -663,7 +664,7 @@ static gtc_status step_pipelined(gtc_ctx* c, const float* grad, float* residual,
         e = cudaEventRecord(c->ev_chunk[i], stream);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_chunk[i], 0);
         if (e != cudaSuccess) return cuda_fail(c, e, "step: chunk event");
-        s = decode_range(c, target, alpha, mode, nullptr, c->side, tb, te, i);
+        s = decode_range(c, target, alpha, mode, nullptr, c->side, tb, te, i, false);
         if (s != GTC_OK) return s;
     }
     e = cudaEventRecord(c->ev_join, c->side);

@@ -47,10 +47,11 @@ struct MsgHeader {
 // The hot path's message is SEGMENTED: encode kernel 1 compacts the words of
 // tile t (ascending index) into slot t of a tile-major buffer,
 //     words of tile t = seg[t * kTile .. t * kTile + count_t),
-// and tag[t] = (epoch << 32) | count_t.  In p2p mode a one-thread publish
-// kernel follows the encode kernel: fence at system scope, then raise
-// Ctrl::ready = step, which peers acquire before reading the message over
-// NVLink.  Decode reads exactly the words of the tiles it owns, from
+// and tag[t] = (epoch << 32) | count_t.  In p2p mode the rank publishes the
+// whole message by raising Ctrl::ready[slot] = step after a system-scope
+// fence -- done by block 0 of its decode kernel (stream order puts every
+// encode store before it), or by a one-thread publish kernel per chunk in the
+// pipelined gtc_step -- and peers acquire that flag before reading over NVLink.  Decode reads exactly the words of the tiles it owns, from
 // every rank, without a global prefix scan.
 // The CONTIGUOUS message (words in one array + per-tile offsets + header) is
 // the wire format of the NCCL exchange and of gtc_message; gtc_compact_kernel
@@ -108,6 +109,7 @@ struct DecodeParams {
     unsigned long long step;       // p2p: wait until every rank's Ctrl::ready >= step
     int wait;                      // segmented p2p: acquire every rank's ready flag first
     const unsigned long long* ready[GTC_MAX_MSGS];  // p2p: each rank's Ctrl::ready
+    unsigned long long* publish;   // p2p: raise this rank's ready flag (= step) first, or null
     int nmsg;
     long long n;
     int num_tiles;
