@@ -44,6 +44,7 @@ namespace {
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kPre = 2;                 // words per thread per message preloaded
 constexpr int kPreMsgs = 8;             // messages whose first words are preloaded
+constexpr int kBatch = 8;               // words loaded per thread before their count updates
 constexpr int kMaxTouched = 2048;       // non-zero counts applied through the list (else dense fallback)
 constexpr int kChunksPerThread = kDecMaxTilesPerCta * (kTile / 16) / kDecThreads;
 constexpr unsigned long long kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000;
@@ -176,6 +177,27 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         return __ldg(p.words[m] + s_beg[m] + f);
     };
 
+    // words [from, len) of message m into the counts, kBatch independent loads
+    // per thread before their shared-memory updates (dense messages would
+    // otherwise pay one memory round trip per word per thread)
+    auto count_words = [&](int m, int from, int len) {
+        for (int f0 = from + tid; f0 < len; f0 += kBatch * kDecThreads) {
+            unsigned w[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int f = f0 + u * kDecThreads;
+                w[u] = f < len ? word_at(m, f) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                if (f0 + u * kDecThreads < len) {
+                    const int local = (int)((w[u] >> 1) - (unsigned)base);
+                    s_cnt[local] = (signed char)(s_cnt[local] + ((w[u] & 1u) ? -1 : 1));
+                }
+            }
+        }
+    };
+
     // preload the first words of the first messages (one memory round trip)
     unsigned pre[kPreMsgs][kPre];
 #pragma unroll
@@ -203,20 +225,11 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
                 s_cnt[local] = (signed char)(s_cnt[local] + ((word & 1u) ? -1 : 1));
             }
         }
-        for (int f = kPre * kDecThreads + tid; f < len; f += kDecThreads) {
-            const unsigned word = word_at(m, f);
-            const int local = (int)((word >> 1) - (unsigned)base);
-            s_cnt[local] = (signed char)(s_cnt[local] + ((word & 1u) ? -1 : 1));
-        }
+        count_words(m, kPre * kDecThreads, len);
         __syncthreads();
     }
     for (int m = kPreMsgs; m < p.nmsg; ++m) {
-        const int len = s_pre(m, nt);
-        for (int f = tid; f < len; f += kDecThreads) {
-            const unsigned word = word_at(m, f);
-            const int local = (int)((word >> 1) - (unsigned)base);
-            s_cnt[local] = (signed char)(s_cnt[local] + ((word & 1u) ? -1 : 1));
-        }
+        count_words(m, 0, s_pre(m, nt));
         __syncthreads();
     }
 

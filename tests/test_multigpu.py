@@ -15,7 +15,7 @@ def ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("cmp", ["gt", "ge"])
 @pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 def test_exchange_parity(world, cmp, exchange):
