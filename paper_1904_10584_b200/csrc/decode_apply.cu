@@ -304,18 +304,55 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
             if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
         }
     } else {
-        // dense batch: each thread applies its own chunks
+        // dense CTA: one list per round u of 256 chunks (4096 counts), each
+        // built by a block scan and applied with independent loads; a round
+        // that alone overflows the list is applied per thread
+        __syncthreads();  // everyone has read s_warp
 #pragma unroll
         for (int u = 0; u < kChunksPerThread; ++u) {
-            unsigned msk = nz[u];
-            const int q = u * kDecThreads + tid;
-            while (msk) {
-                const int b = __ffs(msk) - 1;
-                msk &= msk - 1;
-                const int local = q * 16 + b;
-                const long long gi = base + local;
-                if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
+            const unsigned msk_u = nz[u];
+            const unsigned my_u = __popc(msk_u);
+            unsigned inc = my_u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(kFullMask, inc, o);
+                if (lane >= o) inc += y;
             }
+            if (lane == 31) s_warp[warp] = inc;
+            __syncthreads();
+            unsigned wb = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kDecThreads / 32; ++w) {
+                const unsigned v = s_warp[w];
+                wb += (w < warp) ? v : 0u;
+                tot += v;
+            }
+            const int q = u * kDecThreads + tid;
+            if (tot <= (unsigned)kMaxTouched) {
+                unsigned pos = wb + inc - my_u;
+                unsigned msk = msk_u;
+                while (msk) {
+                    const int b = __ffs(msk) - 1;
+                    msk &= msk - 1;
+                    s_list[pos++] = (unsigned short)(q * 16 + b);
+                }
+                __syncthreads();
+                for (unsigned i = tid; i < tot; i += kDecThreads) {
+                    const int local = s_list[i];
+                    const long long gi = base + local;
+                    if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
+                }
+            } else {
+                unsigned msk = msk_u;
+                while (msk) {
+                    const int b = __ffs(msk) - 1;
+                    msk &= msk - 1;
+                    const int local = q * 16 + b;
+                    const long long gi = base + local;
+                    if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
+                }
+            }
+            __syncthreads();  // s_warp / s_list are reused by the next round
         }
     }
     stamp(5);
