@@ -113,6 +113,10 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         if (trace) g_trace[blockIdx.x * kTracePhases + ph] = globaltimer_ns();
     };
     stamp(0);
+    // programmatic dependent launch: wait for the previous kernel (the encode)
+    // and its memory before touching anything
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     if (p.publish && blockIdx.x == 0 && threadIdx.x == 0) {
         // p2p: every store of this rank's encode precedes this kernel (stream
         // order); make them visible at system scope, then tell the peers
@@ -393,6 +397,8 @@ __device__ __forceinline__ void apply_words(const DecodeParams& p, const unsigne
 // segmented: one warp per tile
 template <int MODE>
 __global__ void __launch_bounds__(kSingleThreads) gtc_apply_single_seg_kernel(const DecodeParams p) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     if (*p.flags & (kFlagCapacity | kFlagCorrupt)) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long stride = (long long)gridDim.x * (kSingleThreads / 32);
@@ -446,6 +452,16 @@ __global__ void gtc_tile_bounds_kernel(const BoundsParams p) {
     if (bad) atomicOr(p.flags, kFlagCorrupt);
 }
 
+// Programmatic dependent launch of the decode kernels (GTC_PDL=0 disables).
+bool pdl_on() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 int sm_count() {
     static int sms = 0;
     if (sms == 0) {
@@ -493,8 +509,17 @@ cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
     if (forced > 0) tpc = forced < kDecMaxTilesPerCta ? forced : kDecMaxTilesPerCta;
     p.tiles_per_cta = tpc;
     const int grid = (range + tpc - 1) / tpc;
-    kern<<<grid, kDecThreads, dyn_smem(tpc), s>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kDecThreads);
+    cfg.dynamicSmemBytes = dyn_smem(tpc);
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 // GTC_DECODE_GENERAL=1 routes one-message decodes through the counting
@@ -514,7 +539,16 @@ cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
         p.tile_end == p.num_tiles) {
         if (p.segmented) {
             const int grid = (int)std::min<long long>((p.num_tiles + 7) / 8, (long long)sm_count() * 8);
-            gtc_apply_single_seg_kernel<MODE><<<grid, kSingleThreads, 0, s>>>(p);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)grid);
+            cfg.blockDim = dim3(kSingleThreads);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, gtc_apply_single_seg_kernel<MODE>, p);
         } else {
             gtc_apply_single_kernel<MODE><<<sm_count() * 8, kSingleThreads, 0, s>>>(p);
         }

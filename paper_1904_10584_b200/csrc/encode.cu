@@ -313,6 +313,13 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
     const long long base = tile * kTile;
     const bool full_tile = base + kTile <= p.n;
 
+    // Programmatic dependent launch: this grid may have been launched while
+    // the previous kernel on the stream (e.g. the previous step) was still
+    // draining; wait for it (and its memory) before touching any data, and let
+    // the next launch begin as early as possible.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+
     float4 rv[kTileVec];
     float4 gv[kTileVec];
     if (full_tile && TMA) {
@@ -611,18 +618,34 @@ int encode_variant() {
 }
 bool use_persistent() { return encode_variant() == 1; }
 
+// Programmatic dependent launch of the encode kernel (GTC_PDL=0 disables).
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int CMP, bool HAS_G>
 cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
     p.chunk_tiles = 1;
     p.num_chunks = p.num_tiles;
     if (p.tile_end <= p.tile_begin) return cudaSuccess;
-    if (encode_variant() == 2) {
-        const size_t smem = (HAS_G ? 2 : 1) * (size_t)kTileBytes;
-        gtc_encode_tile_kernel<CMP, HAS_G, true><<<p.tile_end - p.tile_begin, kTileThreads, smem, s>>>(p);
-    } else {
-        gtc_encode_tile_kernel<CMP, HAS_G, false><<<p.tile_end - p.tile_begin, kTileThreads, 0, s>>>(p);
-    }
-    return cudaGetLastError();
+    const bool tma = encode_variant() == 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.tile_end - p.tile_begin));
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = tma ? (HAS_G ? 2 : 1) * (size_t)kTileBytes : 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return tma ? cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, true>, p)
+               : cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, false>, p);
 }
 
 template <int CMP>
