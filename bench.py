@@ -463,10 +463,11 @@ def run_gtc(args):
 
 
 def run_bmuf(args):
-    """The paper's other trainer: one BMUF-NBM sync step =
-    reduce-scatter of the local models + fused Eqs. (1)-(4) on the rank's shard
-    + all-gather of Wg, timed over K steps; it runs once per block of 100
-    mini-batches (PAPER.md:249)."""
+    """The paper's other trainer: one BMUF-NBM sync step,
+    timed over K steps; it runs once per block of 100 mini-batches
+    (PAPER.md:249).  p2p (default): one kernel reads shard r of every rank's
+    model over NVLink, applies Eqs. (1)-(4) and stores Wg into every model;
+    nccl: reduce-scatter + fused Eqs. (1)-(4) on the shard + all-gather."""
     import torch
     import torch.distributed as dist
 
@@ -481,7 +482,7 @@ def run_bmuf(args):
     eta = args.bmuf_eta if args.bmuf_eta is not None else 1.0 - 1.0 / max(world, 2)
     zeta = gtc.bmuf_zeta(args.bmuf_C, world, eta)
     w0 = torch.from_numpy(synth.normal(n, synth.BASE_SEED, 0, 11)).to(dev)
-    b = gtc.BMUF(n, eta, zeta, rank, world, dev, w_init=w0)
+    b = gtc.BMUF(n, eta, zeta, rank, world, dev, w_init=w0, exchange=args.exchange)
     w = b.local_buffer()
     w[:n].copy_(w0)
     w[:n].add_(torch.from_numpy(synth.normal(n, synth.rank_seed(rank), 1) * np.float32(1e-3)).to(dev))
@@ -503,6 +504,7 @@ def run_bmuf(args):
         b.sync(w)
     e1.record(stream)
     torch.cuda.synchronize()
+    b.check()
     if world > 1:
         dist.barrier()
     clocks.mark()
@@ -514,16 +516,22 @@ def run_bmuf(args):
     ms = ms.item()
     if rank == 0:
         peak, peak_src = measured_peaks()
-        hbm_bytes = 24 * b.shard  # fused kernel: read sum, Wg, Delta; write Wg, Delta, local shard
-        nvl = 2 * (world - 1) * 4 * b.shard  # reduce-scatter + all-gather bytes in and out per rank
+        # own HBM per rank: read + write Wg, Delta and the own model's shard
+        # (nccl: the reduced sum in place of the model); NVLink per rank:
+        # (N-1) shards in + (N-1) shards out, as reduce-scatter + all-gather
+        hbm_bytes = 24 * b.shard
+        nvl = 2 * (world - 1) * 4 * b.shard
+        design = ("one kernel: rank-ordered double mean of shard r over NVLink peer reads -> Eqs. (1)-(4) -> "
+                  "Wg stored into every rank's model (device-side flags, no NCCL)" if b.workspace is not None else
+                  "in-place NCCL reduce-scatter -> fused Eqs. (1)-(4) on the rank's shard -> in-place NCCL "
+                  "all-gather")
         line = {
             "metric": "params/sec BMUF-NBM sync step (Eqs. 1-4)", "value": world * n / (ms * 1e-3),
             "unit": "params/s", "n_gpus": world, "steps": K, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "algo": "bmuf",
             "config": {"workload": args.workload, "n_params": n, "eta": eta, "zeta": zeta, "C": args.bmuf_C,
-                       "shard": b.shard, "design": "in-place NCCL reduce-scatter -> fused Eqs. (1)-(4) on the "
-                                                   "rank's shard -> in-place NCCL all-gather"},
+                       "shard": b.shard, "exchange": b.exchange, "design": design},
             "bytes_per_step": {"hbm_kernel": hbm_bytes, "nvlink_per_rank": nvl},
             "achieved_GBs_if_hbm_only": (hbm_bytes + (2 * 4 * b.shard * (world - 1) if world > 1 else 0))
             / (ms * 1e-3) / 1e9, "peak": peak, "peak_source": peak_src,

@@ -25,9 +25,20 @@
  * on all ranks).  Single GPU, simulated workers (bmuf_sync_sim): the mean is
  * a rank-ordered double sum divided by N, rounded once (the oracle's).
  *
- * Memory: all device pointers are caller-owned; no workspace is needed.
- * Local models are float[padded_len] (padded_len = world * shard_len >= n,
- * shard_len a multiple of 4; the tail beyond n is ignored but moved).
+ * p2p mode (bmuf_bind_workspace; world <= 8, one node): the local models
+ * live in caller-allocated workspaces that are CUDA-IPC mapped on every
+ * rank, and bmuf_sync is ONE kernel with no NCCL call: rank r reads shard r of
+ * every rank's model over NVLink, forms Wbar as the rank-ordered double sum
+ * divided by N, rounded once (the simulated workers' and the oracle's
+ * reading, so the result is bit-exact with oracle_bmuf_step), updates its Wg /
+ * Delta shard and stores the new Wg shard into every rank's model.
+ * Synchronisation is device-side (system-scope release/acquire flags in the
+ * workspaces); a peer that does not arrive within 30 s raises GTC_EPEER,
+ * reported by bmuf_check.
+ *
+ * Memory: all device pointers are caller-owned.  Local models are
+ * float[padded_len] (padded_len = world * shard_len >= n, shard_len a
+ * multiple of 4; the tail beyond n is ignored but moved).
  */
 #ifndef GTC_BMUF_H
 #define GTC_BMUF_H
@@ -62,6 +73,19 @@ int64_t bmuf_padded_len(const bmuf_ctx* ctx);
  * 16-byte aligned pointers. */
 gtc_status bmuf_sync(bmuf_ctx* ctx, float* w_local, float* wg_shard, float* delta_shard, float eta,
                      float zeta, cudaStream_t stream);
+
+/* p2p workspace: *bytes = 4096 + 4 * padded_len.  Binding (collective: every
+ * rank calls it) zeroes the flags, maps every rank's workspace and returns
+ * GTC_EUNSUPPORTED on every rank if any mapping fails (then use NCCL mode:
+ * do not bind).  The workspace (256-byte aligned, caller-owned, from
+ * cudaMalloc or torch's allocator) must outlive the context.  After binding,
+ * bmuf_sync's w_local must be bmuf_model(ctx). */
+gtc_status bmuf_workspace_size(const bmuf_ctx* ctx, size_t* bytes);
+gtc_status bmuf_bind_workspace(bmuf_ctx* ctx, void* workspace, size_t bytes);
+/* The local model inside the bound workspace (float[padded_len]); NULL if unbound. */
+float* bmuf_model(const bmuf_ctx* ctx);
+/* Synchronises the device; GTC_EPEER if a p2p step timed out waiting for a peer. */
+gtc_status bmuf_check(bmuf_ctx* ctx);
 
 /* Simulated workers on one GPU (world == 1 context): nmodels local models
  * (host array of device pointers, float[n] each), full Wg and Delta (float[n]);

@@ -71,6 +71,10 @@ _SIGS = {
     "bmuf_shard_len": (_i64, [_vp]),
     "bmuf_padded_len": (_i64, [_vp]),
     "bmuf_sync": (_i32, [_vp, _vp, _vp, _vp, _f32, _f32, _vp]),
+    "bmuf_workspace_size": (_i32, [_vp, ctypes.POINTER(ctypes.c_size_t)]),
+    "bmuf_bind_workspace": (_i32, [_vp, _vp, ctypes.c_size_t]),
+    "bmuf_model": (_vp, [_vp]),
+    "bmuf_check": (_i32, [_vp]),
     "bmuf_sync_sim": (_i32, [_vp, _vp, _i32, _vp, _vp, _f32, _f32, _vp]),
     "bmuf_zeta": (ctypes.c_double, [ctypes.c_double, _i32, ctypes.c_double]),
     "bmuf_destroy": (None, [_vp]),
@@ -429,6 +433,24 @@ def bmuf_sync(ctx, w_local_ptr: int, wg_shard_ptr: int, delta_shard_ptr: int, et
     _chk(load_library().bmuf_sync(ctx, w_local_ptr, wg_shard_ptr, delta_shard_ptr, eta, zeta, stream), "bmuf_sync")
 
 
+def bmuf_workspace_size(ctx) -> int:
+    b = ctypes.c_size_t(0)
+    _chk(load_library().bmuf_workspace_size(ctx, ctypes.byref(b)), "bmuf_workspace_size")
+    return b.value
+
+
+def bmuf_bind_workspace(ctx, ptr: int, nbytes: int):
+    _chk(load_library().bmuf_bind_workspace(ctx, ptr, nbytes), "bmuf_bind_workspace")
+
+
+def bmuf_model(ctx) -> int:
+    return load_library().bmuf_model(ctx) or 0
+
+
+def bmuf_check(ctx):
+    _chk(load_library().bmuf_check(ctx), "bmuf_check")
+
+
 def bmuf_sync_sim(ctx, w_ptrs, wg_ptr: int, delta_ptr: int, eta: float, zeta: float, stream: int):
     P = (_vp * max(len(w_ptrs), 1))(*w_ptrs)
     _chk(load_library().bmuf_sync_sim(ctx, P, len(w_ptrs), wg_ptr, delta_ptr, eta, zeta, stream), "bmuf_sync_sim")
@@ -446,10 +468,15 @@ def bmuf_destroy(ctx):
 class BMUF:
     """One rank's BMUF-NBM synchroniser.  Holds this rank's
     shard of the global model Wg and of the block momentum Delta (torch-owned);
-    ``sync(w_local)`` runs Eqs. (1)-(4) and leaves Wg(t) in ``w_local``."""
+    ``sync(w_local)`` runs Eqs. (1)-(4) and leaves Wg(t) in ``w_local``.
+
+    exchange="p2p" (default): the local model lives in an IPC-mapped workspace
+    (``local_buffer()`` returns it) and a step is one kernel over NVLink,
+    bit-exact with the oracle; "nccl": reduce-scatter + kernel + all-gather on
+    any caller buffer of ``padded`` elements."""
 
     def __init__(self, n_params: int, eta: float, zeta: float, rank: int = 0, world: int = 1, device=None,
-                 group=None, w_init=None):
+                 group=None, w_init=None, exchange: str = "p2p"):
         import torch
 
         if not torch.cuda.is_available():
@@ -464,6 +491,18 @@ class BMUF:
         self.padded = bmuf_padded_len(self.ctx)
         self.wg = torch.zeros(self.shard, dtype=torch.float32, device=self.device)
         self.delta = torch.zeros(self.shard, dtype=torch.float32, device=self.device)
+        if exchange not in ("p2p", "nccl"):
+            raise ValueError("exchange must be 'p2p' or 'nccl'")
+        self.exchange = exchange
+        self.workspace = None
+        if exchange == "p2p":
+            nbytes = bmuf_workspace_size(self.ctx)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            with torch.cuda.device(self.device):
+                bmuf_bind_workspace(self.ctx, self.workspace.data_ptr(), nbytes)
+            off = bmuf_model(self.ctx) - self.workspace.data_ptr()
+            self._model = self.workspace[off:off + 4 * self.padded].view(torch.float32)
+            self._model.zero_()
         if w_init is not None:  # Wg(0): this rank's shard of the initial model
             lo = self.rank * self.shard
             hi = min(self.n, lo + self.shard)
@@ -471,14 +510,22 @@ class BMUF:
                 self.wg[: hi - lo].copy_(w_init.reshape(-1)[lo:hi])
 
     def local_buffer(self):
-        """A zero-padded float[padded_len] buffer for the local model."""
+        """The float[padded_len] local model buffer (p2p: the one in the
+        workspace, zeroed at construction; nccl: a new zeroed tensor)."""
         import torch
 
+        if self.workspace is not None:
+            return self._model
         return torch.zeros(self.padded, dtype=torch.float32, device=self.device)
+
+    def check(self):
+        bmuf_check(self.ctx)
 
     def sync(self, w_local, stream=None):
         if w_local.numel() != self.padded:
             raise ValueError("w_local must have bmuf_padded_len elements")
+        if self.workspace is not None and w_local.data_ptr() != self._model.data_ptr():
+            raise ValueError("p2p BMUF: w_local must be local_buffer()")
         bmuf_sync(self.ctx, _ptr(w_local, "w_local"), _ptr(self.wg, "wg"), _ptr(self.delta, "delta"),
                   self.eta, self.zeta, _stream(stream, self.device))
 

@@ -10,14 +10,29 @@
 // Simulated workers (one GPU): one kernel reads every model in rank order
 // (double accumulator, the oracle's reading B3), updates Wg and Delta and
 // writes Wg back into every model.
+//
+// world > 1 with a bound workspace (p2p, the default of the Python binding):
+// the local models live in CUDA-IPC-mapped workspaces and ONE kernel per step
+// does the whole exchange over NVLink -- rank r reads its shard of every
+// rank's model in rank order (the simulated workers' double mean, bit-exact
+// with the oracle), updates its Wg / Delta shard and stores the new Wg shard
+// straight into every rank's model.  Handshake (system-scope release /
+// acquire on flags in the workspaces): block 0 raises this rank's ready(t)
+// (its model is final); every CTA waits for all ready(t) before reading; the
+// last CTA to finish (device-scope arrival counter) raises pushed[rank](t) in
+// every peer's flags and waits until every peer has pushed into this rank's
+// model.  NVLink bytes per rank are those of RS + AG; there is no NCCL call
+// and no second pass over HBM.
 #include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "bmuf.h"
+#include "gtc_internal.cuh"
 
 namespace {
 
@@ -73,6 +88,143 @@ __global__ void __launch_bounds__(kThreads) bmuf_sim_kernel(SimModels m, int nm,
     }
 }
 
+// ---------------------------------------------------------------- p2p step
+constexpr int kMaxRanks = 8;
+constexpr unsigned long long kTimeoutNs = 30ull * 1000 * 1000 * 1000;
+
+// Workspace: [flags 0..1023 | IPC records 1024..2047 | pad | model float[padded]]
+struct Flags {
+    unsigned long long ready;               // this rank's model is final for step t
+    unsigned long long pad0[7];
+    unsigned long long pushed[kMaxRanks];   // pushed[i]: rank i has stored its Wg shard here
+    unsigned int done;                      // CTAs of this rank's kernel that finished
+    int error;                              // 1: a peer timed out
+};
+constexpr size_t kIpcOff = 1024;
+constexpr size_t kModelOff = 4096;
+static_assert(sizeof(Flags) <= kIpcOff, "flags fit");
+static_assert(kIpcOff + gtc::kIpcRecordBytes * kMaxRanks <= kModelOff, "IPC records fit");
+
+struct P2PParams {
+    float* model[kMaxRanks];              // every rank's model (own included), shard offset applied
+    Flags* flags[kMaxRanks];              // every rank's flags
+    float* wg;
+    float* delta;
+    long long len4;
+    int rank, world;
+    float eta, zeta;
+    unsigned long long step;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ bool wait_at_least(const unsigned long long* a, unsigned long long step) {
+    unsigned long long v = ld_acquire_sys(a);
+    if (v >= step) return true;
+    const unsigned long long t0 = globaltimer_ns();
+    while (v < step) {
+        if (globaltimer_ns() - t0 > kTimeoutNs) return false;
+        __nanosleep(128);
+        v = ld_acquire_sys(a);
+    }
+    return true;
+}
+
+// fl(sum / W): division by a power of two is the exact product with 1/W
+template <int W>
+__device__ __forceinline__ float mean_of(double sum) {
+    if constexpr ((W & (W - 1)) == 0) return __double2float_rn(__dmul_rn(sum, 1.0 / W));
+    else return __double2float_rn(__ddiv_rn(sum, (double)W));
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, 3) bmuf_p2p_kernel(const P2PParams p) {
+    __shared__ int s_abort;
+    Flags* own = p.flags[p.rank];
+    if (threadIdx.x == 0) {
+        s_abort = 0;
+        if (blockIdx.x == 0) {  // this rank's model (written by earlier kernels on the stream) is final
+            __threadfence_system();
+            st_release_sys(&own->ready, p.step);
+        }
+    }
+    __syncthreads();
+    // ready(t) of every rank; a peer is at most one step ahead (its next step
+    // waits for this rank's pushes), hence >=
+    if (threadIdx.x < p.world && !wait_at_least(&p.flags[threadIdx.x]->ready, p.step)) {
+        s_abort = 1;
+        atomicExch(&own->error, 1);
+    }
+    __syncthreads();
+    if (!s_abort) {
+        // U float4 per thread per iteration, all W * U loads issued up front
+        // (the remote ones cross NVLink: latency-bound without enough in flight)
+        constexpr int U = W <= 4 ? 2 : 1;
+        const long long stride = (long long)gridDim.x * kThreads;
+        for (long long q0 = (long long)blockIdx.x * kThreads + threadIdx.x; q0 < p.len4; q0 += stride * U) {
+            float4 v[U][W];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int i = 0; i < W; ++i)
+                    if (q0 + u * stride < p.len4)
+                        v[u][i] = __ldcg(reinterpret_cast<const float4*>(p.model[i]) + q0 + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long q = q0 + u * stride;
+                if (q >= p.len4) break;
+                // Eq. (1): rank-ordered double sum, divided by N, rounded once (B3)
+                double ax = 0.0, ay = 0.0, az = 0.0, aw = 0.0;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    ax = __dadd_rn(ax, (double)v[u][i].x);
+                    ay = __dadd_rn(ay, (double)v[u][i].y);
+                    az = __dadd_rn(az, (double)v[u][i].z);
+                    aw = __dadd_rn(aw, (double)v[u][i].w);
+                }
+                float4 g = reinterpret_cast<const float4*>(p.wg)[q];
+                float4 d = reinterpret_cast<const float4*>(p.delta)[q];
+                bmuf_elem(mean_of<W>(ax), g.x, d.x, p.eta, p.zeta);
+                bmuf_elem(mean_of<W>(ay), g.y, d.y, p.eta, p.zeta);
+                bmuf_elem(mean_of<W>(az), g.z, d.z, p.eta, p.zeta);
+                bmuf_elem(mean_of<W>(aw), g.w, d.w, p.eta, p.zeta);
+                reinterpret_cast<float4*>(p.wg)[q] = g;
+                reinterpret_cast<float4*>(p.delta)[q] = d;
+#pragma unroll
+                for (int i = 0; i < W; ++i) __stcg(reinterpret_cast<float4*>(p.model[i]) + q, g);
+            }
+        }
+    }
+    // last CTA of this rank: publish the pushes, then wait for every peer's
+    __syncthreads();
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned prev = atomicAdd(&own->done, 1u);
+        s_last = (prev == gridDim.x - 1);
+        if (s_last) {
+            own->done = 0;
+            __threadfence_system();
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (threadIdx.x < p.world) st_release_sys(&p.flags[threadIdx.x]->pushed[p.rank], p.step);
+    __syncthreads();
+    if (threadIdx.x < p.world && !wait_at_least(&own->pushed[threadIdx.x], p.step)) atomicExch(&own->error, 1);
+}
+
 int sm_count() {
     static int sms = 0;
     if (sms == 0) {
@@ -91,7 +243,41 @@ struct bmuf_ctx {
     long long n = 0, shard = 0;
     int rank = 0, world = 1, device = 0;
     ncclComm_t comm = nullptr;
+    // p2p (bmuf_bind_workspace)
+    unsigned char* ws = nullptr;
+    std::vector<unsigned char*> peer_ws;
+    std::vector<void*> peer_alloc;
+    unsigned long long steps = 0;
+    int grid = 0;
+    void (*kernel)(P2PParams) = nullptr;
 };
+
+namespace {
+Flags* flags_of(unsigned char* ws) { return reinterpret_cast<Flags*>(ws); }
+float* model_of(unsigned char* ws) { return reinterpret_cast<float*>(ws + kModelOff); }
+size_t workspace_bytes(const bmuf_ctx* c) { return kModelOff + sizeof(float) * (size_t)c->shard * c->world; }
+
+using P2PKernel = void (*)(P2PParams);
+P2PKernel p2p_kernel(int world) {
+    switch (world) {
+        case 1: return bmuf_p2p_kernel<1>;
+        case 2: return bmuf_p2p_kernel<2>;
+        case 3: return bmuf_p2p_kernel<3>;
+        case 4: return bmuf_p2p_kernel<4>;
+        case 5: return bmuf_p2p_kernel<5>;
+        case 6: return bmuf_p2p_kernel<6>;
+        case 7: return bmuf_p2p_kernel<7>;
+        default: return bmuf_p2p_kernel<8>;
+    }
+}
+
+// one resident wave: every CTA spins on the ready flags at once
+int p2p_grid(P2PKernel k) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreads, 0) != cudaSuccess || per < 1) per = 1;
+    return per * sm_count();
+}
+}  // namespace
 
 extern "C" {
 
@@ -130,16 +316,98 @@ gtc_status bmuf_init(bmuf_ctx** out, int64_t n, int rank, int world, const void*
 int64_t bmuf_shard_len(const bmuf_ctx* c) { return c ? c->shard : 0; }
 int64_t bmuf_padded_len(const bmuf_ctx* c) { return c ? c->shard * c->world : 0; }
 
+gtc_status bmuf_workspace_size(const bmuf_ctx* c, size_t* bytes) {
+    if (!c || !bytes) return GTC_EINVAL;
+    if (c->world > kMaxRanks) return GTC_EUNSUPPORTED;
+    *bytes = workspace_bytes(c);
+    return GTC_OK;
+}
+
+gtc_status bmuf_bind_workspace(bmuf_ctx* c, void* workspace, size_t bytes) {
+    if (!c || !workspace) return GTC_EINVAL;
+    if (c->ws) return GTC_ESTATE;
+    if (c->world > kMaxRanks) return GTC_EUNSUPPORTED;
+    if (bytes < workspace_bytes(c)) return GTC_ECAPACITY;
+    if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return GTC_EALIGN;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != c->device) cudaSetDevice(c->device);
+    unsigned char* ws = static_cast<unsigned char*>(workspace);
+    gtc_status st = GTC_OK;
+    if (cudaMemset(ws, 0, kModelOff) != cudaSuccess) st = GTC_ECUDA;
+    if (st == GTC_OK && c->world > 1) {
+        switch (gtc::ipc_map_peers(c->comm, c->rank, c->world, ws, workspace_bytes(c), ws + kIpcOff, c->peer_ws,
+                                   c->peer_alloc)) {
+            case gtc::IpcResult::kOk: break;
+            case gtc::IpcResult::kCudaError: st = GTC_ECUDA; break;
+            case gtc::IpcResult::kNcclError: st = GTC_ENCCL; break;
+            default: st = GTC_EUNSUPPORTED;
+        }
+        // the IPC records overlapped nothing live; clear the flags again
+        if (st == GTC_OK && cudaMemset(ws, 0, kModelOff) != cudaSuccess) st = GTC_ECUDA;
+        // no rank may start a step before every rank has cleared its flags
+        if (st == GTC_OK) {
+            int* one = reinterpret_cast<int*>(ws + kIpcOff);
+            if (ncclAllReduce(one, one, 1, ncclInt32, ncclSum, c->comm, 0) != ncclSuccess ||
+                cudaStreamSynchronize(0) != cudaSuccess)
+                st = GTC_ENCCL;
+        }
+    } else if (st == GTC_OK) {
+        c->peer_ws.assign(1, ws);
+        c->peer_alloc.assign(1, nullptr);
+    }
+    if (st == GTC_OK) {
+        c->ws = ws;
+        c->steps = 0;
+        c->kernel = p2p_kernel(c->world);
+        c->grid = p2p_grid(c->kernel);
+    }
+    if (prev != c->device) cudaSetDevice(prev);
+    return st;
+}
+
+float* bmuf_model(const bmuf_ctx* c) { return (c && c->ws) ? model_of(c->ws) : nullptr; }
+
+gtc_status bmuf_check(bmuf_ctx* c) {
+    if (!c) return GTC_EINVAL;
+    if (!c->ws) return GTC_OK;
+    int err = 0;
+    if (cudaMemcpy(&err, &flags_of(c->ws)->error, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return GTC_ECUDA;
+    return err ? GTC_EPEER : GTC_OK;
+}
+
 gtc_status bmuf_sync(bmuf_ctx* c, float* w_local, float* wg_shard, float* delta_shard, float eta, float zeta,
                      cudaStream_t stream) {
     if (!c) return GTC_EINVAL;
     if (c->shard > 0 && (!w_local || !wg_shard || !delta_shard)) return GTC_EINVAL;
     if (!aligned16(w_local) || !aligned16(wg_shard) || !aligned16(delta_shard)) return GTC_EALIGN;
     if (!std::isfinite(eta) || !std::isfinite(zeta)) return GTC_EINVAL;
+    if (c->ws && w_local != model_of(c->ws)) return GTC_EINVAL;  // p2p: the model lives in the workspace
     if (c->shard == 0) return GTC_OK;
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != c->device) cudaSetDevice(c->device);
+    if (c->ws) {
+        P2PParams p{};
+        const size_t off = (size_t)c->rank * (size_t)c->shard;
+        for (int i = 0; i < c->world; ++i) {
+            p.model[i] = model_of(c->peer_ws[i]) + off;
+            p.flags[i] = flags_of(c->peer_ws[i]);
+        }
+        p.wg = wg_shard;
+        p.delta = delta_shard;
+        p.len4 = c->shard / 4;
+        p.rank = c->rank;
+        p.world = c->world;
+        p.eta = eta;
+        p.zeta = zeta;
+        p.step = ++c->steps;
+        c->kernel<<<c->grid, kThreads, 0, stream>>>(p);
+        const cudaError_t e = cudaGetLastError();
+        if (prev != c->device) cudaSetDevice(prev);
+        return e == cudaSuccess ? GTC_OK : GTC_ECUDA;
+    }
     float* mine = w_local + (size_t)c->rank * (size_t)c->shard;
     gtc_status st = GTC_OK;
     if (c->world > 1 &&
@@ -184,6 +452,13 @@ double bmuf_zeta(double C, int N, double eta) { return C * (double)N * (1.0 - et
 
 void bmuf_destroy(bmuf_ctx* c) {
     if (!c) return;
+    if (c->comm && c->ws && c->world > 1) {  // no peer may still be reading or pushing into this workspace
+        cudaSetDevice(c->device);
+        cudaDeviceSynchronize();
+        int* one = reinterpret_cast<int*>(c->ws + kIpcOff);
+        if (ncclAllReduce(one, one, 1, ncclInt32, ncclSum, c->comm, 0) == ncclSuccess) cudaStreamSynchronize(0);
+        gtc::ipc_unmap(c->peer_alloc);
+    }
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }

@@ -15,7 +15,6 @@
 //   nccl (GTC_EXCHANGE_NCCL): the message is packed contiguously, then
 //        ncclAllGather of (k, flags), one host wait for the largest k,
 //        ncclAllGather of the words and tile offsets.
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -55,7 +54,7 @@ struct Layout {
     size_t ipc, kx_all, recv, recv_off, sim_off, total;
 };
 
-constexpr size_t kIpcRecord = 128;
+constexpr size_t kIpcRecord = kIpcRecordBytes;
 
 Layout make_layout(long long n, int world, bool p2p, long long capacity, int max_sim_msgs) {
     const long long tiles = (n + kTile - 1) / kTile;
@@ -88,14 +87,6 @@ Layout make_layout(long long n, int world, bool p2p, long long capacity, int max
     return L;
 }
 
-struct IpcRecord {
-    cudaIpcMemHandle_t handle;   // 64 B, of the allocation holding the workspace
-    unsigned long long offset;   // workspace base - allocation base
-    unsigned long long total;    // layout size (must agree on every rank)
-    int ok;                      // this rank could export its workspace
-    int device;
-};
-static_assert(sizeof(IpcRecord) <= kIpcRecord, "IPC record fits its slot");
 
 }  // namespace
 
@@ -184,89 +175,18 @@ unsigned char* rank_ws(const gtc_ctx* c, int rank) {
     return (c->world > 1 && c->p2p) ? c->peer_ws[rank] : c->ws;
 }
 
-// Base address of the allocation holding p (driver API, resolved at run time
-// so that libgtc.so does not link libcuda).
-typedef int (*MemGetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
-
-bool allocation_base(const void* p, unsigned long long* base) {
-    static MemGetAddressRangeFn fn = nullptr;
-    if (!fn) {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !f)
-            return false;
-        fn = reinterpret_cast<MemGetAddressRangeFn>(f);
-    }
-    size_t size = 0;
-    return fn(base, &size, reinterpret_cast<unsigned long long>(p)) == 0;
-}
-
-// p2p: export this rank's workspace, all-gather the records over NCCL, map
-// every peer's workspace.  All ranks agree on the outcome.
+// p2p: map every peer's workspace (ipc.cu); all ranks agree on the outcome.
 gtc_status connect_peers(gtc_ctx* c) {
-    IpcRecord rec{};
-    unsigned long long base = 0;
-    rec.ok = allocation_base(c->ws, &base) &&
-             cudaIpcGetMemHandle(&rec.handle, reinterpret_cast<void*>(base)) == cudaSuccess;
-    cudaGetLastError();
-    rec.offset = rec.ok ? reinterpret_cast<unsigned long long>(c->ws) - base : 0ull;
-    rec.total = c->L.total;
-    rec.device = c->device;
-    unsigned char* slots = c->ws + c->L.ipc;
-    cudaError_t e = cudaMemcpy(slots + kIpcRecord * c->rank, &rec, sizeof(rec), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ipc record");
-    ncclResult_t r = ncclAllGather(slots + kIpcRecord * c->rank, slots, kIpcRecord, ncclUint8, c->comm, 0);
-    if (r != ncclSuccess) return nccl_fail(c, r, "bind: ncclAllGather(ipc)");
-    e = cudaStreamSynchronize(0);
-    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ipc sync");
-    std::vector<unsigned char> all(kIpcRecord * c->world);
-    e = cudaMemcpy(all.data(), slots, all.size(), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ipc readback");
-    c->peer_ws.assign(c->world, nullptr);
-    c->peer_alloc.assign(c->world, nullptr);
-    int ok = 1;
-    for (int i = 0; i < c->world; ++i) {
-        IpcRecord ri;
-        std::memcpy(&ri, all.data() + kIpcRecord * i, sizeof(ri));
-        if (!ri.ok || ri.total != c->L.total) ok = 0;
+    const IpcResult r = ipc_map_peers(c->comm, c->rank, c->world, c->ws, c->L.total, c->ws + c->L.ipc, c->peer_ws,
+                                      c->peer_alloc);
+    switch (r) {
+        case IpcResult::kOk: return GTC_OK;
+        case IpcResult::kCudaError: return fail(c, GTC_ECUDA, "bind: CUDA IPC exchange");
+        case IpcResult::kNcclError: return fail(c, GTC_ENCCL, "bind: NCCL IPC exchange");
+        default:
+            return fail(c, GTC_EUNSUPPORTED,
+                        "p2p exchange: workspaces cannot be mapped across ranks (use GTC_EXCHANGE_NCCL)");
     }
-    if (ok) {
-        for (int i = 0; i < c->world; ++i) {
-            if (i == c->rank) {
-                c->peer_ws[i] = c->ws;
-                continue;
-            }
-            IpcRecord ri;
-            std::memcpy(&ri, all.data() + kIpcRecord * i, sizeof(ri));
-            void* p = nullptr;
-            if (cudaIpcOpenMemHandle(&p, ri.handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-                cudaGetLastError();
-                ok = 0;
-                break;
-            }
-            c->peer_alloc[i] = p;
-            c->peer_ws[i] = static_cast<unsigned char*>(p) + ri.offset;
-        }
-    }
-    // agree: every rank must have mapped every peer
-    int* okd = reinterpret_cast<int*>(slots);
-    e = cudaMemcpy(okd + c->rank, &ok, sizeof(int), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ok flag");
-    r = ncclAllGather(okd + c->rank, okd, 1, ncclInt32, c->comm, 0);
-    if (r != ncclSuccess) return nccl_fail(c, r, "bind: ncclAllGather(ok)");
-    std::vector<int> oks(c->world, 0);
-    e = cudaMemcpy(oks.data(), okd, sizeof(int) * c->world, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(c, e, "bind: ok readback");
-    for (int v : oks) ok &= v;
-    if (!ok) {
-        for (void* p : c->peer_alloc)
-            if (p) cudaIpcCloseMemHandle(p);
-        c->peer_alloc.assign(c->world, nullptr);
-        return fail(c, GTC_EUNSUPPORTED,
-                    "p2p exchange: workspaces cannot be mapped across ranks (use GTC_EXCHANGE_NCCL)");
-    }
-    return GTC_OK;
 }
 
 // Pack rank `rank`'s segmented message of the current step into this rank's
@@ -897,8 +817,7 @@ void gtc_destroy(gtc_ctx* c) {
         if (c->ev_join) cudaEventDestroy(c->ev_join);
         cudaStreamDestroy(c->side);
     }
-    for (void* p : c->peer_alloc)
-        if (p) cudaIpcCloseMemHandle(p);
+    ipc_unmap(c->peer_alloc);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->host_kx) cudaFreeHost(c->host_kx);
     delete c;

@@ -4,7 +4,10 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
+
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include "gtc.h"
 
@@ -132,6 +135,14 @@ struct BoundsParams {
     int num_tiles;
     unsigned long long* flags;
 };
+
+// CUDA-IPC mapping of one buffer per rank (ipc.cu).  `slots` is device
+// scratch of kIpcRecordBytes * world bytes; `tag` must agree on all ranks.
+constexpr int kIpcRecordBytes = 128;
+enum class IpcResult { kOk, kCudaError, kNcclError, kUnsupported };
+IpcResult ipc_map_peers(ncclComm_t comm, int rank, int world, unsigned char* local, unsigned long long tag,
+                        unsigned char* slots, std::vector<unsigned char*>& peers, std::vector<void*>& allocs);
+void ipc_unmap(std::vector<void*>& allocs);
 
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);

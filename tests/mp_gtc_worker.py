@@ -96,19 +96,32 @@ def bmuf_main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
+    exchange = os.environ.get("GTC_EXCHANGE", "p2p")
     eta = 1.0 - 1.0 / world
     zeta = 1.0  # Eq. (5) with C = 1
     w0 = synth.normal(n, 5)
-    b = gtc.BMUF(n, eta, zeta, rank, world, dev, w_init=torch.from_numpy(w0).to(dev))
+    b = gtc.BMUF(n, eta, zeta, rank, world, dev, w_init=torch.from_numpy(w0).to(dev), exchange=exchange)
     wg_h, d_h = w0.copy(), np.zeros(n, np.float32)
     w = b.local_buffer()
     eps = np.float64(2.0 ** -24)
+    lo = rank * b.shard
+    hi = min(n, lo + b.shard)
     for t in range(4):
         ws_h = [(wg_h + synth.normal(n, 20 + i, t) * np.float32(0.01)).astype(np.float32) for i in range(world)]
         w[:n].copy_(torch.from_numpy(ws_h[rank]))
+        if t % 2 == 1:  # ranks arrive at different times: the device-side waits must hold
+            torch.cuda._sleep(int(2e6 * rank))
         b.sync(w)
         torch.cuda.synchronize()
+        b.check()
         got = w[:n].cpu().numpy()
+        if exchange == "p2p":  # rank-ordered double mean: bit-exact with the oracle
+            wg_o, d_o = wg_h.copy(), d_h.copy()
+            oracle.bmuf_step([x.copy() for x in ws_h], wg_o, d_o, eta, zeta)
+            assert np.array_equal(got.view(np.uint32), wg_o.view(np.uint32)), f"rank {rank} step {t}: Wg differs"
+            assert np.array_equal(b.delta[: hi - lo].cpu().numpy().view(np.uint32), d_o[lo:hi].view(np.uint32)), \
+                f"rank {rank} step {t}: Delta differs"
+            assert np.array_equal(b.wg[: hi - lo].cpu().numpy().view(np.uint32), wg_o[lo:hi].view(np.uint32))
         wg_prev = wg_h.astype(np.float64)
         d_prev = d_h.astype(np.float64)
         mean_abs = np.mean(np.abs(np.stack(ws_h).astype(np.float64)), axis=0)
@@ -127,18 +140,34 @@ def bmuf_main():
         bad = np.argmax(err - tol)
         assert np.all(err <= tol), f"rank {rank} step {t}: err {err[bad]} vs tol {tol[bad]} at {bad}"
         wg_h = got.copy()  # continue from the device state (each step checked on its own)
-        lo = rank * b.shard
-        hi = min(n, lo + b.shard)
         d_dev = b.delta[: hi - lo].cpu().numpy()
         d_h[lo:hi] = d_dev  # likewise for Delta
         hs = [None] * world
         dist.all_gather_object(hs, hashlib.sha256(got.tobytes()).hexdigest())
         assert len(set(hs)) == 1, f"ranks disagree on Wg at step {t}"
+    if exchange == "p2p":
+        # back-to-back steps with device-side local updates and no host sync:
+        # the push / ready handshake alone orders them
+        wg_o, d_o = wg_h.copy(), d_h.copy()
+        ws_o = [wg_o.copy() for _ in range(world)]
+        w[:n].copy_(torch.from_numpy(wg_h))
+        for t in range(3):
+            x = [(synth.normal(n, 40 + i, t) * np.float32(0.01)).astype(np.float32) for i in range(world)]
+            w[:n].add_(torch.from_numpy(x[rank]).to(dev, non_blocking=True))
+            torch.cuda._sleep(int(1e6 * ((rank + t) % world)))
+            b.sync(w)
+            ws_o = [(ws_o[i] + x[i]).astype(np.float32) for i in range(world)]
+            oracle.bmuf_step(ws_o, wg_o, d_o, eta, zeta)
+            ws_o = [wg_o.copy() for _ in range(world)]
+        torch.cuda.synchronize()
+        b.check()
+        assert np.array_equal(w[:n].cpu().numpy().view(np.uint32), wg_o.view(np.uint32)), \
+            f"rank {rank}: back-to-back steps differ from the oracle"
     b.close()
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
-        print(f"BMUF OK world={world} n={n}")
+        print(f"BMUF OK world={world} n={n} exchange={exchange}")
 
 
 if __name__ == "__main__":

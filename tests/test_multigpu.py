@@ -40,11 +40,14 @@ def test_exchange_lstm_am_size(exchange):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
 
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_bmuf_multigpu(world):
+def test_bmuf_multigpu(world, exchange):
+    """p2p: bit-exact with oracle_bmuf_step at every step, also back to back
+    without host syncs; nccl: within the derived rounding bound."""
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, GTC_MODE="bmuf", GTC_N="1000003")
+    env = dict(os.environ, GTC_MODE="bmuf", GTC_N="1000003", GTC_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
