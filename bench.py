@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--alpha", type=float, default=-1e-3, help="apply scale (e.g. -lr)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="world > 1: NVLink peer reads fused into decode (p2p) or NCCL all-gather")
+    ap.add_argument("--accum", choices=["weights", "momentum"], default="weights",
+                    help="apply: sparse fmaf into the weights (headline) or the dense SGD-momentum update")
+    ap.add_argument("--mu", type=float, default=0.9, help="SGD momentum for --accum momentum")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -157,7 +160,16 @@ def make_inputs(n, tau, rho, rank, world):
 
 
 # ------------------------------------------------------------------ oracle legs
-def cpu_oracle_run(n_full, tau, rho, cmp, alpha, budget_s, world=1, inputs=None):
+def oracle_step_args(args_accum, mu, n):
+    """(accum_mode, extra kwargs) of oracle.step for --accum."""
+    import oracle
+
+    if args_accum == "momentum":
+        return oracle.ACCUM_MOMENTUM, {"buf": np.zeros(n, np.float32), "mu": mu}
+    return oracle.ACCUM_WEIGHTS, {}
+
+
+def cpu_oracle_run(n_full, tau, rho, cmp, alpha, budget_s, world=1, inputs=None, accum="weights", mu=0.9):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
     import oracle
 
@@ -168,11 +180,12 @@ def cpu_oracle_run(n_full, tau, rho, cmp, alpha, budget_s, world=1, inputs=None)
     rs = [r0.copy() for _ in range(world)]
     w = w0.copy()
     mode = oracle.CMP_GT if cmp == "gt" else oracle.CMP_GE
+    amode, akw = oracle_step_args(accum, mu, n)
     steps, t_used = 0, 0.0
     while t_used < budget_s or steps < 1:
         g = [gs[steps % len(gs)]] * world
         t0 = time.perf_counter()
-        oracle.step(g, rs, w, tau, mode, alpha, oracle.ACCUM_WEIGHTS)
+        oracle.step(g, rs, w, tau, mode, alpha, amode, **akw)
         t_used += time.perf_counter() - t0
         steps += 1
         if steps >= 200:
@@ -199,11 +212,12 @@ def run_reference(args):
     mode = oracle.CMP_GT if args.cmp == "gt" else oracle.CMP_GE
     rs = [r0.copy() for _ in range(world)]
     w = w0.copy()
+    amode, akw = oracle_step_args(args.accum, args.mu, n)
     for t in range(args.warmup):
-        oracle.step([grads[t % len(grads)]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
+        oracle.step([grads[t % len(grads)]] * world, rs, w, args.tau, mode, args.alpha, amode, **akw)
     t0 = time.perf_counter()
     for t in range(args.steps):
-        oracle.step([grads[t % len(grads)]] * world, rs, w, args.tau, mode, args.alpha, oracle.ACCUM_WEIGHTS)
+        oracle.step([grads[t % len(grads)]] * world, rs, w, args.tau, mode, args.alpha, amode, **akw)
     dt = time.perf_counter() - t0
     value = world * n * args.steps / dt
     sample = f"each step: {n} of {n_full} params x {world} simulated worker(s), oracle.step single thread"
@@ -212,7 +226,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": args.workload, "n_params": n_full, "sample_params": n,
-                                        "tau": args.tau, "rho_target": args.rho, "cmp": args.cmp},
+                                        "tau": args.tau, "rho_target": args.rho, "cmp": args.cmp,
+                                        "apply": "ACCUM_MOMENTUM" if args.accum == "momentum" else "ACCUM_WEIGHTS"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -247,11 +262,16 @@ def run_gtc(args):
     cap = 0 if n < 100_000_000 or args.exchange == "nccl" else n // 20
     ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp, exchange=args.exchange, max_words_per_rank=cap)
     stream = torch.cuda.current_stream(dev)
+    momentum = args.accum == "momentum"
+    amode = gtc.GTC_ACCUM_MOMENTUM if momentum else gtc.GTC_ACCUM_WEIGHTS
+    if momentum:
+        mbuf = torch.zeros(n, dtype=torch.float32, device=dev)
+        ctx.bind_momentum(mbuf, args.mu)
 
     def step(t):
         ctx.encode(grads[t % NB], r)
         ctx.exchange()
-        ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
+        ctx.decode_apply(w, args.alpha, amode)
 
     for t in range(max(3, args.warmup)):
         step(t)
@@ -264,7 +284,7 @@ def run_gtc(args):
     # three separate calls with events between them (per-kernel durations).
     K = args.steps
     EV_EVERY = 8
-    stepf = ctx.stepper(grads, r, w, args.alpha, gtc.GTC_ACCUM_WEIGHTS, stream)
+    stepf = ctx.stepper(grads, r, w, args.alpha, amode, stream)
     inst = [t for t in range(K) if t % EV_EVERY == 0]
     ev = {t: [torch.cuda.Event(enable_timing=True) for _ in range(4)] for t in inst}
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -292,7 +312,7 @@ def run_gtc(args):
                 e[1].record(stream)
                 ctx.exchange()
                 e[2].record(stream)
-                ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
+                ctx.decode_apply(w, args.alpha, amode)
                 e[3].record(stream)
         else:
             stepf(t)
@@ -323,7 +343,7 @@ def run_gtc(args):
             ctx.encode(grads[t % NB], r)
             eb[t][1].record(stream)
             ctx.exchange()
-            ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS)
+            ctx.decode_apply(w, args.alpha, amode)
             eb[t][2].record(stream)
         torch.cuda.synchronize()
         brk = {"encode_only_ms": sum(e[0].elapsed_time(e[1]) for e in eb) / B,
@@ -333,7 +353,7 @@ def run_gtc(args):
     cnt = torch.empty(n, dtype=torch.int8, device=dev)
     ctx.encode(grads[K % NB], r)
     ctx.exchange()
-    ctx.decode_apply(w, args.alpha, gtc.GTC_ACCUM_WEIGHTS, cnt)
+    ctx.decode_apply(w, args.alpha, amode, cnt)
     nnz_c = int(torch.count_nonzero(cnt).item())
     k_all = ctx.last_counts()
     del cnt
@@ -360,7 +380,7 @@ def run_gtc(args):
         E = args.e2e_steps
         for t in range(2):
             gdev.copy_(pinned[t % NB], non_blocking=True)
-            ctx.step(gdev, r, w, args.alpha)
+            ctx.step(gdev, r, w, args.alpha, amode)
             k_host.copy_(ctx.local_count_tensor(), non_blocking=True)
             torch.cuda.synchronize()
         if world > 1:
@@ -370,7 +390,7 @@ def run_gtc(args):
         s0.record(stream)
         for t in range(E):
             gdev.copy_(pinned[t % NB], non_blocking=True)
-            ctx.step(gdev, r, w, args.alpha)
+            ctx.step(gdev, r, w, args.alpha, amode)
             k_host.copy_(ctx.local_count_tensor(), non_blocking=True)
             stream.synchronize()
             _ = int(k_host[0])
@@ -398,14 +418,16 @@ def run_gtc(args):
     if world == 1:
         # the fused step kernel: stream g, r -> r (12 B/param), words (4 k),
         # tags (8 B/tile), target read-modify-write of the k touched elements
-        enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles + 8 * k_rank
+        enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles + (16 * n if momentum else 8 * k_rank)
         kernel_name = "gtc_encode_tile_kernel (fused apply, world 1)"
     else:
         enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles
         kernel_name = "gtc_encode_tile_kernel"
     enc_gbs = enc_bytes / (enc_ms * 1e-3) / 1e9
     sum_k = sum(k_all)
-    dec_bytes = 4 * sum_k + 8 * world * ntiles + 8 * nnz_c
+    # decode: words + tags read, then the apply (sparse: 8 B per non-zero
+    # count; momentum: w and buf read and written, 16 B per parameter)
+    dec_bytes = 4 * sum_k + 8 * world * ntiles + (16 * n if momentum else 8 * nnz_c)
     dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9 if world > 1 and dec_ms > 0 else None
     step_bytes = enc_bytes + (dec_bytes + 4 * (world - 1) * max(k_all) if world > 1 else 0)
     traffic = None
@@ -422,7 +444,7 @@ def run_gtc(args):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_oracle_run(n, tau, args.rho, args.cmp, args.alpha, args.cpu_seconds,
-                             inputs=(grads_h, r0_h.copy(), w0_h.copy()))
+                             inputs=(grads_h, r0_h.copy(), w0_h.copy()), accum=args.accum, mu=args.mu)
 
     value = world * n / (ms_per_step * 1e-3)
     line = {
@@ -431,7 +453,8 @@ def run_gtc(args):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.workload, "desc": wl["desc"], "n_params": n, "tau": tau,
                    "rho_target": args.rho, "rho_measured": k_rank / n, "cmp": args.cmp,
-                   "parallelism": f"dp{world}", "apply": "ACCUM_WEIGHTS",
+                   "parallelism": f"dp{world}",
+                   "apply": f"ACCUM_MOMENTUM (mu={args.mu})" if momentum else "ACCUM_WEIGHTS",
                    "exchange": ctx.exchange_mode(),
                    "l2": f"inputs larger than L2: g rotates over {NB} buffer(s), "
                          f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},

@@ -92,9 +92,13 @@ enum { GTC_EXCHANGE_P2P = 0,     /* default: peers' messages are read straight f
        GTC_EXCHANGE_NCCL = 16    /* ncclAllGather of counts, one host wait, then
                                     ncclAllGather of the words and tile offsets  */ };
 
-/* What decode_apply updates (R8). */
+/* What decode_apply updates (R8, M1). */
 enum { GTC_ACCUM_WEIGHTS = 0, /* target[i] = fmaf(alpha, fl(c[i]*tau), target[i]) */
-       GTC_ACCUM_UPDATE = 1   /* target[i] = fl(target[i] + fl(c[i]*tau))        */ };
+       GTC_ACCUM_UPDATE = 1,  /* target[i] = fl(target[i] + fl(c[i]*tau))        */
+       GTC_ACCUM_MOMENTUM = 2 /* SGD with momentum, EVERY i (M1):
+                                 buf[i] = fl(fl(mu*buf[i]) + fl(c[i]*tau));
+                                 target[i] = fmaf(alpha, buf[i], target[i]);
+                                 buf / mu from gtc_bind_momentum, alpha = -lr  */ };
 
 /* Most messages one decode_apply can aggregate (ranks or simulated workers). */
 #define GTC_MAX_MSGS 64
@@ -170,11 +174,22 @@ gtc_status gtc_exchange(gtc_ctx* ctx, cudaStream_t stream);
  * nothing is applied and gtc_check reports it): signed integer counts of all ranks' quanta
  * (deterministic, atomic-free, rank order irrelevant) and the apply of
  * count * tau to target (float[n] device, in/out) for every element with a
- * non-zero count (mode GTC_ACCUM_WEIGHTS with alpha, or GTC_ACCUM_UPDATE).
+ * non-zero count (mode GTC_ACCUM_WEIGHTS with alpha, or GTC_ACCUM_UPDATE), or
+ * the momentum update of every element (GTC_ACCUM_MOMENTUM; GTC_ESTATE if no
+ * buffer is bound).
  * counts_out: int8[n] device or NULL; if given receives every count (debug /
  * parity; costs n extra bytes written). */
 gtc_status gtc_decode_apply(gtc_ctx* ctx, float* target, float alpha, int mode,
                             int8_t* counts_out, cudaStream_t stream);
+
+/* Optimizer state of mode GTC_ACCUM_MOMENTUM (the SGD step
+ * after the path, in SPEC:82-85's form buf' = mu*buf + grad, params' =
+ * params - lr*buf'): buf is float[n] device (caller-owned, 16-byte aligned,
+ * zero at the start of training), mu finite.  The apply is dense (every
+ * element's momentum decays), 16 B/param more than the sparse modes; at
+ * world 1 gtc_step fuses it into the encode kernel.  buf = NULL unbinds.
+ * Returns GTC_EINVAL / GTC_EALIGN on bad arguments. */
+gtc_status gtc_bind_momentum(gtc_ctx* ctx, float* buf, float mu);
 
 /* One whole step: gtc_encode, gtc_exchange, gtc_decode_apply in one call
  * (same arguments and semantics; returns the first failing status, or

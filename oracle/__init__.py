@@ -24,6 +24,7 @@ CMP_GT = 0
 CMP_GE = 1
 ACCUM_WEIGHTS = 0
 ACCUM_UPDATE = 1
+ACCUM_MOMENTUM = 2  # the same value as GTC_ACCUM_MOMENTUM; oracle.step's own dispatch
 
 OK, EDIM, EINVAL, ECORRUPT = 0, 1, 2, 3
 
@@ -57,6 +58,8 @@ def lib():
         L.oracle_encode.argtypes = [i64, f32, i32, vp, vp, vp,
                                     ctypes.POINTER(i64), ctypes.POINTER(i32)]
         L.oracle_encode.restype = i32
+        L.oracle_apply_momentum.argtypes = [i64, f32, vp, vp, vp, f32, f32]
+        L.oracle_apply_momentum.restype = i32
         L.oracle_decode_counts.argtypes = [i64, i32, vp, vp, vp]
         L.oracle_decode_counts.restype = i32
         L.oracle_apply.argtypes = [i64, f32, vp, vp, f32, i32]
@@ -129,12 +132,36 @@ def apply(counts, target, tau: float, alpha: float = 1.0, accum_mode: int = ACCU
     return target
 
 
+def apply_momentum(counts, w, buf, tau: float, alpha: float, mu: float):
+    """SGD-momentum apply of the aggregate (reading M1): for every i,
+    buf = fl(fl(mu*buf) + fl(c*tau)); w = fmaf(alpha, buf, w).  In place."""
+    counts = np.ascontiguousarray(counts, dtype=np.int32)
+    _f32(w, "w")
+    _f32(buf, "buf")
+    if not (counts.size == w.size == buf.size):
+        raise ValueError("counts, w and buf differ in size")
+    st = lib().oracle_apply_momentum(w.size, float(tau), _ptr(counts), _ptr(w), _ptr(buf), float(alpha), float(mu))
+    if st != OK:
+        raise OracleError(st, "apply_momentum")
+    return w
+
+
 def step(gs, rs, target, tau: float, cmp_mode: int = CMP_GT, alpha: float = 1.0,
-         accum_mode: int = ACCUM_WEIGHTS):
+         accum_mode: int = ACCUM_WEIGHTS, buf=None, mu: float = 0.0):
     """One synchronous GTC step over len(rs) simulated workers.
 
-    ``rs`` and ``target`` are updated in place.  Returns
-    ``(messages list[uint32 array], counts int32[n], nonfinite bool)``."""
+    ``rs`` and ``target`` (and ``buf`` for ACCUM_MOMENTUM) are updated in
+    place.  Returns ``(messages list[uint32 array], counts int32[n], nonfinite bool)``."""
+    if accum_mode == ACCUM_MOMENTUM:
+        # encode every worker, aggregate, then the momentum apply (all steps in liboracle)
+        msgs, nfs = [], False
+        for w, r in enumerate(rs):
+            m, nf = encode(gs[w] if gs is not None else None, r, tau, cmp_mode)
+            msgs.append(m)
+            nfs |= nf
+        counts = decode_counts(msgs, target.size)
+        apply_momentum(counts, target, buf, tau, alpha, mu)
+        return msgs, counts, nfs
     nw = len(rs)
     n = target.size
     for r in rs:

@@ -108,6 +108,24 @@ int oracle_apply(int64_t n, float tau, const int32_t* counts,
     return ORACLE_OK;
 }
 
+int oracle_apply_momentum(int64_t n, float tau, const int32_t* counts,
+                          float* w, float* buf, float alpha, float mu)
+{
+    int st = oracle_check_args(n, tau);
+    if (st != ORACLE_OK) return st;
+    if (!isfinite(mu) || !isfinite(alpha)) return ORACLE_EINVAL;
+    /* SPEC:85 "buf' = momentum*buf + grad; params' = params - lr*buf'" with
+     * grad = the aggregate c[i] quanta of tau, alpha = -lr (M1). */
+    for (int64_t i = 0; i < n; ++i) {
+        float u = (float)counts[i] * tau;
+        float b = mu * buf[i];
+        b = b + u;
+        buf[i] = b;
+        w[i] = fmaf(alpha, b, w[i]);
+    }
+    return ORACLE_OK;
+}
+
 int oracle_step(int64_t n, float tau, int cmp_mode, int nworkers,
                 const float* const* g, float* const* r,
                 uint32_t* const* words, int64_t* ks,

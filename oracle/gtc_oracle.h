@@ -76,6 +76,17 @@ int oracle_decode_counts(int64_t n, int nmsg,
 int oracle_apply(int64_t n, float tau, const int32_t* counts,
                  float* target, float alpha, int accum_mode);
 
+/* Step 6b with the SGD-momentum update (reading M1): the
+ * aggregate is the gradient of an SGD step with momentum, "stochastic
+ * gradient descent (SGD)", in SPEC:82-85's form buf' = mu*buf + grad,
+ * params' = params - lr*buf' (alpha = -lr, as in ACCUM_WEIGHTS).  For EVERY i
+ * (the decaying momentum moves untouched weights too):
+ *   u = fl((float)c[i] * tau)          (+0 where c[i] == 0)
+ *   buf[i] = fl(fl(mu * buf[i]) + u)
+ *   w[i]   = fmaf(alpha, buf[i], w[i])                                   */
+int oracle_apply_momentum(int64_t n, float tau, const int32_t* counts,
+                          float* w, float* buf, float alpha, float mu);
+
 /* One synchronous GTC step for nworkers simulated workers ("we select
  * the synchronous variant"):  every worker encodes its own g/r, all messages
  * are "received" by everyone (concatenation in rank order), counts are

@@ -39,6 +39,7 @@ GTC_EXCHANGE_P2P = 0
 GTC_EXCHANGE_NCCL = 16
 GTC_ACCUM_WEIGHTS = 0
 GTC_ACCUM_UPDATE = 1
+GTC_ACCUM_MOMENTUM = 2
 GTC_MAX_MSGS = 64
 GTC_TILE = 4096
 
@@ -54,6 +55,7 @@ _SIGS = {
     "gtc_exchange": (_i32, [_vp, _vp]),
     "gtc_decode_apply": (_i32, [_vp, _vp, _f32, _i32, _vp, _vp]),
     "gtc_step": (_i32, [_vp, _vp, _vp, _vp, _f32, _i32, _vp]),
+    "gtc_bind_momentum": (_i32, [_vp, _vp, _f32]),
     "gtc_decode_apply_msgs": (_i32, [_vp, _vp, _vp, _i32, _vp, _f32, _i32, _vp, _vp]),
     "gtc_last_counts": (_i32, [_vp, _vp]),
     "gtc_local_count": (_i32, [_vp, ctypes.POINTER(_vp)]),
@@ -159,6 +161,10 @@ def gtc_step(ctx, grad_ptr: int | None, residual_ptr: int, target_ptr: int, alph
     """encode + exchange + decode_apply; returns GTC_OK or GTC_ENONFINITE."""
     return _chk(load_library().gtc_step(ctx, grad_ptr, residual_ptr, target_ptr, alpha, mode, stream),
                 "gtc_step", ctx, ok=(GTC_OK, GTC_ENONFINITE))
+
+
+def gtc_bind_momentum(ctx, buf_ptr: int | None, mu: float):
+    _chk(load_library().gtc_bind_momentum(ctx, buf_ptr, mu), "gtc_bind_momentum", ctx)
 
 
 def gtc_decode_apply_msgs(ctx, msg_ptrs, counts, target_ptr: int, alpha: float, mode: int,
@@ -292,6 +298,16 @@ class GTC:
             nbytes = gtc_workspace_size(self.ctx, max_words_per_rank, max_sim_msgs)
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             gtc_bind_workspace(self.ctx, self.workspace.data_ptr(), nbytes, max_words_per_rank, max_sim_msgs)
+
+    # --- optimizer state (GTC_ACCUM_MOMENTUM)
+    def bind_momentum(self, buf, mu: float):
+        """SGD-momentum state for mode GTC_ACCUM_MOMENTUM (float32[n] device
+        tensor, zero at the start; ``None`` unbinds).  The tensor must outlive
+        its use."""
+        if buf is not None and buf.numel() != self.n:
+            raise ValueError("momentum buffer length != n_params")
+        self._mom = buf
+        gtc_bind_momentum(self.ctx, _ptr(buf, "buf") if buf is not None else None, float(mu))
 
     # --- the three calls of a step
     def encode(self, grad, residual, stream=None):

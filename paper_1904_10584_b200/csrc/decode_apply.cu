@@ -95,6 +95,57 @@ __device__ __forceinline__ void apply_one(const DecodeParams& p, long long gi, i
     p.target[gi] = (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, u, t) : __fadd_rn(t, u);
 }
 
+// buf = fl(fl(mu * buf) + fl(c * tau)); w = fmaf(alpha, buf, w)  (M1)
+__device__ __forceinline__ void momentum_one(float& w, float& b, int c, const DecodeParams& p) {
+    const float u = __fmul_rn((float)c, p.tau);
+    b = __fadd_rn(__fmul_rn(p.mu, b), u);
+    w = __fmaf_rn(p.alpha, b, w);
+}
+
+__device__ __forceinline__ int count_byte(int packed, int e) {
+    return (int)(signed char)((unsigned)packed >> (8 * e));
+}
+
+// elements [base, base + nt * kTile) of target / buf, counts in shared memory
+// (4 int8 per int)
+__device__ __forceinline__ void dense_momentum(const DecodeParams& p, const int* s_cnt_q, long long base, int nt) {
+    constexpr int kU = 4;
+    const int nv = nt * (kTile / 4);
+    float4* w4 = reinterpret_cast<float4*>(p.target + base);
+    float4* b4 = reinterpret_cast<float4*>(p.buf + base);
+    const long long rem = p.n - base;  // elements of this CTA that exist
+    for (int v0 = threadIdx.x; v0 < nv; v0 += kU * kDecThreads) {
+        float4 w[kU], b[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int v = v0 + u * kDecThreads;
+            if (v < nv && 4ll * v + 4 <= rem) {
+                w[u] = __ldcs(w4 + v);
+                b[u] = __ldcs(b4 + v);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int v = v0 + u * kDecThreads;
+            if (v >= nv || 4ll * v >= rem) continue;
+            const int packed = s_cnt_q[v];
+            if (4ll * v + 4 <= rem) {
+                momentum_one(w[u].x, b[u].x, count_byte(packed, 0), p);
+                momentum_one(w[u].y, b[u].y, count_byte(packed, 1), p);
+                momentum_one(w[u].z, b[u].z, count_byte(packed, 2), p);
+                momentum_one(w[u].w, b[u].w, count_byte(packed, 3), p);
+                __stcs(w4 + v, w[u]);
+                __stcs(b4 + v, b[u]);
+            } else {
+                for (int e = 0; 4ll * v + e < rem; ++e) {
+                    const long long gi = base + 4ll * v + e;
+                    momentum_one(p.target[gi], p.buf[gi], count_byte(packed, e), p);
+                }
+            }
+        }
+    }
+}
+
 template <int MODE, bool SEG>
 __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const DecodeParams p) {
     // dynamic shared memory: int8 counts [tiles_per_cta * kTile] | per message
@@ -251,6 +302,14 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
                     if (i0 + e < p.n) p.counts_out[i0 + e] = c[e];
             }
         }
+    }
+
+    if constexpr (MODE == GTC_ACCUM_MOMENTUM) {
+        // SGD-momentum (M1): dense over the CTA's elements -- every momentum
+        // decays -- with 4 float4 of target and of buf in flight per thread
+        dense_momentum(p, reinterpret_cast<const int*>(s_cnt), base, nt);
+        stamp(5);
+        return;
     }
 
     // sparse apply through a list of the non-zero counts
@@ -535,8 +594,8 @@ bool force_general() {
 
 template <int MODE>
 cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
-    if (p.nmsg == 1 && p.counts_out == nullptr && !p.wait && !force_general() && p.tile_begin == 0 &&
-        p.tile_end == p.num_tiles) {
+    if (MODE != GTC_ACCUM_MOMENTUM && p.nmsg == 1 && p.counts_out == nullptr && !p.wait && !force_general() &&
+        p.tile_begin == 0 && p.tile_end == p.num_tiles) {
         if (p.segmented) {
             const int grid = (int)std::min<long long>((p.num_tiles + 7) / 8, (long long)sm_count() * 8);
             cudaLaunchConfig_t cfg = {};
@@ -561,6 +620,7 @@ cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
 
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s) {
     if (p.num_tiles == 0) return cudaSuccess;
+    if (accum_mode == GTC_ACCUM_MOMENTUM) return launch_mode<GTC_ACCUM_MOMENTUM>(p, s);
     return accum_mode == GTC_ACCUM_UPDATE ? launch_mode<GTC_ACCUM_UPDATE>(p, s) : launch_mode<GTC_ACCUM_WEIGHTS>(p, s);
 }
 

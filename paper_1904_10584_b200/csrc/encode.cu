@@ -299,7 +299,16 @@ __device__ __forceinline__ float4 ld_v4(const float4* p) {
 // TMA = true: the tile's r (and g) arrive by two 16 KB 1-D bulk copies into
 // shared memory (one mbarrier), so the loads in flight do not occupy
 // registers and more CTAs fit per SM (GTC_ENCODE_VARIANT=tma).
-template <int CMP, bool HAS_G, bool TMA>
+// fused SGD-momentum apply (world 1, GTC_ACCUM_MOMENTUM; reading M1): for
+// every element, u = fl(c * tau) with c in {-1, 0, +1}, buf = fl(fl(mu * buf) + u),
+// w = fmaf(alpha, buf, w)
+__device__ __forceinline__ void momentum_elem(float& w, float& b, int c, float tau, float alpha, float mu) {
+    const float u = __fmul_rn((float)c, tau);
+    b = __fadd_rn(__fmul_rn(mu, b), u);
+    w = __fmaf_rn(alpha, b, w);
+}
+
+template <int CMP, bool HAS_G, bool TMA, bool MOM>
 __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_kernel(const EncodeParams p) {
     __shared__ unsigned s_scan[kTileVec * kTileWarps];
     __shared__ unsigned s_total;
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
     int eb[kEarly];
     float tv[kEarly];
     unsigned late = 0u;
-    if (p.target) {
+    if (!MOM && p.target) {
         unsigned rem = sel;
 #pragma unroll
         for (int q = 0; q < kEarly; ++q) {
@@ -462,7 +471,46 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
             }
         }
     }
-    if (p.target && sel) {
+    if (MOM) {
+        // dense momentum apply over the whole tile: 16 B/param more
+        if (full_tile) {
+            float4* w4 = reinterpret_cast<float4*>(p.target + base);
+            float4* b4 = reinterpret_cast<float4*>(p.buf + base);
+            float4 wv[kTileVec], bv[kTileVec];
+#pragma unroll
+            for (int j = 0; j < kTileVec; ++j) {
+                wv[j] = ld_v4(w4 + j * kTileThreads + tid);
+                bv[j] = ld_v4(b4 + j * kTileThreads + tid);
+            }
+#pragma unroll
+            for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int b = j * 4 + e;
+                    const int c = ((sel >> b) & 1u) ? (((neg >> b) & 1u) ? -1 : 1) : 0;
+                    float wf = comp(wv[j], e), bf = comp(bv[j], e);
+                    momentum_elem(wf, bf, c, tau, p.alpha, p.mu);
+                    set_comp(wv[j], e, wf);
+                    set_comp(bv[j], e, bf);
+                }
+                w4[j * kTileThreads + tid] = wv[j];
+                b4[j * kTileThreads + tid] = bv[j];
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const long long i = base + (long long)(j * kTileThreads + tid) * 4 + e;
+                    if (i < p.n) {
+                        const int b = j * 4 + e;
+                        const int c = ((sel >> b) & 1u) ? (((neg >> b) & 1u) ? -1 : 1) : 0;
+                        momentum_elem(p.target[i], p.buf[i], c, tau, p.alpha, p.mu);
+                    }
+                }
+            }
+        }
+    } else if (p.target && sel) {
         // world 1 fused apply (loads issued early, see above): c = +-1 on the
         // selected elements, fl(+-1 * tau) = +-tau, target = fmaf(alpha, +-tau,
         // target) (R8) -- identical to decode_apply.
@@ -644,8 +692,12 @@ cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return tma ? cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, true>, p)
-               : cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, false>, p);
+    if (p.target && p.accum_mode == GTC_ACCUM_MOMENTUM) {
+        cfg.dynamicSmemBytes = 0;
+        return cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, false, true>, p);
+    }
+    return tma ? cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, true, false>, p)
+               : cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, false, false>, p);
 }
 
 template <int CMP>

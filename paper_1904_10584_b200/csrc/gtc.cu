@@ -116,6 +116,8 @@ struct gtc_ctx {
     std::vector<void*> peer_alloc;  // what cudaIpcOpenMemHandle returned (to close)
     unsigned epoch = 0;             // step counter: tag stamp; parity selects the p2p buffer
     unsigned long long encodes = 0; // encodes since bind (the step value of the p2p ready flags)
+    float* mom_buf = nullptr;       // GTC_ACCUM_MOMENTUM state (gtc_bind_momentum)
+    float mom_mu = 0.f;
     cudaStream_t side = nullptr;    // p2p gtc_step pipeline: decode chunks run here
     cudaEvent_t ev_chunk[kMaxPipe] = {};
     cudaEvent_t ev_join = nullptr;
@@ -381,6 +383,8 @@ static gtc_status encode_range(gtc_ctx* c, const float* grad, float* residual, c
     p.target = fused_target;
     p.alpha = fused_alpha;
     p.accum_mode = fused_mode;
+    p.buf = c->mom_buf;
+    p.mu = c->mom_mu;
     p.epoch = c->epoch;
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     p.num_tiles = c->num_tiles;
@@ -487,7 +491,19 @@ gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
 static gtc_status check_apply_args(gtc_ctx* c, float* target, int mode) {
     if (c->n > 0 && !target) return fail(c, GTC_EINVAL, "decode_apply: target is null");
     if (!aligned16(target)) return fail(c, GTC_EALIGN, "decode_apply: target alignment");
-    if (mode != GTC_ACCUM_WEIGHTS && mode != GTC_ACCUM_UPDATE) return fail(c, GTC_EINVAL, "decode_apply: mode");
+    if (mode != GTC_ACCUM_WEIGHTS && mode != GTC_ACCUM_UPDATE && mode != GTC_ACCUM_MOMENTUM)
+        return fail(c, GTC_EINVAL, "decode_apply: mode");
+    if (mode == GTC_ACCUM_MOMENTUM && c->n > 0 && !c->mom_buf)
+        return fail(c, GTC_ESTATE, "decode_apply: GTC_ACCUM_MOMENTUM needs gtc_bind_momentum");
+    return GTC_OK;
+}
+
+gtc_status gtc_bind_momentum(gtc_ctx* c, float* buf, float mu) {
+    if (!c) return GTC_EINVAL;
+    if (!std::isfinite(mu)) return fail(c, GTC_EINVAL, "bind_momentum: mu not finite");
+    if (!aligned16(buf)) return fail(c, GTC_EALIGN, "bind_momentum: buffer alignment");
+    c->mom_buf = buf;
+    c->mom_mu = mu;
     return GTC_OK;
 }
 
@@ -525,6 +541,8 @@ static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode,
     p.tau = c->tau;
     p.alpha = alpha;
     p.target = target;
+    p.buf = c->mom_buf;
+    p.mu = c->mom_mu;
     p.counts_out = reinterpret_cast<signed char*>(counts_out);
     p.flags = &c->ctrl->flags;
     p.trace = decode_trace_enabled() ? 1 : 0;
@@ -673,6 +691,8 @@ gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const 
     p.tau = c->tau;
     p.alpha = alpha;
     p.target = target;
+    p.buf = c->mom_buf;
+    p.mu = c->mom_mu;
     p.counts_out = reinterpret_cast<signed char*>(counts_out);
     p.flags = &c->ctrl->flags;
     e = launch_decode_apply(p, mode, stream);

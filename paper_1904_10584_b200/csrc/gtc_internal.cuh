@@ -76,6 +76,8 @@ struct EncodeParams {
     float* target;                 // world 1 fused apply (gtc_step): null = no apply
     float alpha;
     int accum_mode;
+    float* buf;                    // GTC_ACCUM_MOMENTUM: momentum buffer [n]
+    float mu;
     unsigned epoch;
     int publish_sys;               // p2p: peers read this message over NVLink
     unsigned long long step;       // p2p: encodes since bind (the value raised in Ctrl::ready)
@@ -120,6 +122,8 @@ struct DecodeParams {
     float tau;
     float alpha;
     float* target;
+    float* buf;                    // GTC_ACCUM_MOMENTUM: momentum buffer [n] (dense apply)
+    float mu;
     signed char* counts_out;       // may be null
     unsigned long long* flags;     // this rank's Ctrl::flags
     int tiles_per_cta;             // set by launch_decode_apply

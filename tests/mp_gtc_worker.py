@@ -28,6 +28,10 @@ def main():
     steps = int(os.environ.get("GTC_STEPS", 4))
     cmp = os.environ.get("GTC_CMP", "gt")
     exchange = os.environ.get("GTC_EXCHANGE", "p2p")
+    momentum = os.environ.get("GTC_ACCUM", "weights") == "momentum"
+    gmode = gtc.GTC_ACCUM_MOMENTUM if momentum else gtc.GTC_ACCUM_WEIGHTS
+    omode = oracle.ACCUM_MOMENTUM if momentum else oracle.ACCUM_WEIGHTS
+    mu = 0.9
     tau = 8.0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -43,15 +47,24 @@ def main():
     wd = torch.from_numpy(w0.copy()).to(dev)
     cnt = torch.empty(n, dtype=torch.int8, device=dev)
     mode = oracle.CMP_GT if cmp == "gt" else oracle.CMP_GE
+    buf_or = np.zeros(n, np.float32)
+    bd = torch.zeros(n, dtype=torch.float32, device=dev)
+    if momentum:
+        ctx.bind_momentum(bd, mu)
+
+    def check_buf(what):
+        if momentum:
+            assert np.array_equal(bd.cpu().numpy().view(np.uint32), buf_or.view(np.uint32)), what
     for t in range(steps):
         gs = [synth.correlated_gradient(n, 4.0, synth.BASE_SEED, t, w) for w in range(world)]
         ctx.encode(torch.from_numpy(gs[rank]).to(dev), rd)
         st = ctx.exchange()
         assert st == gtc.GTC_OK, st
         assert ctx.check() == gtc.GTC_OK
-        ctx.decode_apply(wd, -0.5, gtc.GTC_ACCUM_WEIGHTS, cnt)
+        ctx.decode_apply(wd, -0.5, gmode, cnt)
         torch.cuda.synchronize()
-        om, oc, _ = oracle.step(gs, r_or, w_or, tau, mode, -0.5, oracle.ACCUM_WEIGHTS)
+        om, oc, _ = oracle.step(gs, r_or, w_or, tau, mode, -0.5, omode, buf=buf_or, mu=mu)
+        check_buf(f"rank {rank} step {t}: momentum buffer")
         assert ctx.last_counts() == [m.size for m in om], (ctx.last_counts(), [m.size for m in om])
         for w in range(world):
             got = ctx.read_message(w)
@@ -67,10 +80,11 @@ def main():
     # the one-call step (p2p: pipelined encode/decode chunks on two streams)
     for t in range(steps, 2 * steps):
         gs = [synth.correlated_gradient(n, 4.0, synth.BASE_SEED, t, w) for w in range(world)]
-        st = ctx.step(torch.from_numpy(gs[rank]).to(dev), rd, wd, -0.5, gtc.GTC_ACCUM_WEIGHTS)
+        st = ctx.step(torch.from_numpy(gs[rank]).to(dev), rd, wd, -0.5, gmode)
         assert st == gtc.GTC_OK, st
         torch.cuda.synchronize()
-        oracle.step(gs, r_or, w_or, tau, mode, -0.5, oracle.ACCUM_WEIGHTS)
+        oracle.step(gs, r_or, w_or, tau, mode, -0.5, omode, buf=buf_or, mu=mu)
+        check_buf(f"rank {rank} step {t}: momentum buffer (gtc_step)")
         assert np.array_equal(rd.cpu().numpy().view(np.uint32), r_or[rank].view(np.uint32)), f"step {t}: residual"
         wh = wd.cpu().numpy()
         assert np.array_equal(wh.view(np.uint32), w_or.view(np.uint32)), f"step {t}: weights (gtc_step)"
@@ -82,7 +96,7 @@ def main():
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
-        print(f"MULTIGPU OK world={world} n={n} steps={steps} cmp={cmp} exchange={exchange}")
+        print(f"MULTIGPU OK world={world} n={n} steps={steps} cmp={cmp} exchange={exchange} momentum={momentum}")
 
 
 

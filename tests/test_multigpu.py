@@ -40,6 +40,23 @@ def test_exchange_lstm_am_size(exchange):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
 
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_momentum_multigpu(world, exchange):
+    """GTC_ACCUM_MOMENTUM (SGD-momentum apply, reading M1): weights, momentum
+    buffer, residuals, messages and counts bit-exact with the oracle; also the
+    pipelined one-call step."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="3", GTC_N="1000003", GTC_EXCHANGE=exchange,
+               GTC_ACCUM="momentum", GTC_PIPELINE_CHUNKS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29535", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "momentum=True" in p.stdout
+
+
 @pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_bmuf_multigpu(world, exchange):
