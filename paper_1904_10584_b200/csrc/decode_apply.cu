@@ -95,6 +95,36 @@ __device__ __forceinline__ void apply_one(const DecodeParams& p, long long gi, i
     p.target[gi] = (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(p.alpha, u, t) : __fadd_rn(t, u);
 }
 
+// The listed non-zero counts, kApplyBatch independent target loads per
+// thread before their stores (the listed indices are distinct).
+constexpr int kApplyBatch = 4;
+template <int MODE, typename GlobalOf>
+__device__ __forceinline__ void apply_list(const DecodeParams& p, const unsigned short* list, const signed char* cnt,
+                                           unsigned total, const GlobalOf& global_of) {
+    for (unsigned i0 = threadIdx.x; i0 < total; i0 += kApplyBatch * kDecThreads) {
+        long long gi[kApplyBatch];
+        int c[kApplyBatch];
+        float t[kApplyBatch];
+#pragma unroll
+        for (int u = 0; u < kApplyBatch; ++u) {
+            const unsigned i = i0 + u * kDecThreads;
+            gi[u] = -1;
+            if (i < total) {
+                const int local = list[i];
+                const long long g = global_of(local);
+                if (g < p.n) {
+                    gi[u] = g;
+                    c[u] = cnt[local];
+                    t[u] = p.target[g];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kApplyBatch; ++u)
+            if (gi[u] >= 0) apply_one<MODE>(p, gi[u], c[u], t[u]);
+    }
+}
+
 // buf = fl(fl(mu * buf) + fl(c * tau)); w = fmaf(alpha, buf, w)  (M1)
 __device__ __forceinline__ void momentum_one(float& w, float& b, int c, const DecodeParams& p) {
     const float u = __fmul_rn((float)c, p.tau);
@@ -106,41 +136,40 @@ __device__ __forceinline__ int count_byte(int packed, int e) {
     return (int)(signed char)((unsigned)packed >> (8 * e));
 }
 
-// elements [base, base + nt * kTile) of target / buf, counts in shared memory
-// (4 int8 per int)
-__device__ __forceinline__ void dense_momentum(const DecodeParams& p, const int* s_cnt_q, long long base, int nt) {
+// every element of the CTA's tiles (slot i = tile t0 + i * G) of target / buf,
+// counts in shared memory (4 int8 per int), kU float4 of each in flight per thread
+__device__ __forceinline__ void dense_momentum(const DecodeParams& p, const int* s_cnt_q, int t0, int G, int nt) {
     constexpr int kU = 4;
-    const int nv = nt * (kTile / 4);
-    float4* w4 = reinterpret_cast<float4*>(p.target + base);
-    float4* b4 = reinterpret_cast<float4*>(p.buf + base);
-    const long long rem = p.n - base;  // elements of this CTA that exist
+    constexpr int kV = kTile / 4;  // float4 per tile
+    const int nv = nt * kV;
+    float4* w4 = reinterpret_cast<float4*>(p.target);
+    float4* b4 = reinterpret_cast<float4*>(p.buf);
     for (int v0 = threadIdx.x; v0 < nv; v0 += kU * kDecThreads) {
         float4 w[kU], b[kU];
+        long long e0[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int v = v0 + u * kDecThreads;
-            if (v < nv && 4ll * v + 4 <= rem) {
-                w[u] = __ldcs(w4 + v);
-                b[u] = __ldcs(b4 + v);
+            e0[u] = v < nv ? ((long long)t0 + (long long)(v / kV) * G) * kTile + 4ll * (v % kV) : p.n;
+            if (e0[u] + 4 <= p.n) {
+                w[u] = __ldcs(w4 + e0[u] / 4);
+                b[u] = __ldcs(b4 + e0[u] / 4);
             }
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const int v = v0 + u * kDecThreads;
-            if (v >= nv || 4ll * v >= rem) continue;
-            const int packed = s_cnt_q[v];
-            if (4ll * v + 4 <= rem) {
+            if (e0[u] >= p.n) continue;
+            const int packed = s_cnt_q[v0 + u * kDecThreads];
+            if (e0[u] + 4 <= p.n) {
                 momentum_one(w[u].x, b[u].x, count_byte(packed, 0), p);
                 momentum_one(w[u].y, b[u].y, count_byte(packed, 1), p);
                 momentum_one(w[u].z, b[u].z, count_byte(packed, 2), p);
                 momentum_one(w[u].w, b[u].w, count_byte(packed, 3), p);
-                __stcs(w4 + v, w[u]);
-                __stcs(b4 + v, b[u]);
+                __stcs(w4 + e0[u] / 4, w[u]);
+                __stcs(b4 + e0[u] / 4, b[u]);
             } else {
-                for (int e = 0; 4ll * v + e < rem; ++e) {
-                    const long long gi = base + 4ll * v + e;
-                    momentum_one(p.target[gi], p.buf[gi], count_byte(packed, e), p);
-                }
+                for (int e = 0; e0[u] + e < p.n; ++e)
+                    momentum_one(p.target[e0[u] + e], p.buf[e0[u] + e], count_byte(packed, e), p);
             }
         }
     }
@@ -149,12 +178,14 @@ __device__ __forceinline__ void dense_momentum(const DecodeParams& p, const int*
 template <int MODE, bool SEG>
 __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const DecodeParams p) {
     // dynamic shared memory: int8 counts [tiles_per_cta * kTile] | per message
-    // the words before each of its tiles [nmsg][tiles_per_cta + 1] | first word [nmsg]
+    // the words before each of its tiles [nmsg][tiles_per_cta + 1] | contiguous
+    // messages: the first word of each tile [nmsg][tiles_per_cta]
     extern __shared__ int4 s_cnt4[];
     const int npre = p.tiles_per_cta + 1;
     int* s_pre_flat = reinterpret_cast<int*>(reinterpret_cast<signed char*>(s_cnt4) + p.tiles_per_cta * kTile);
-    int* s_beg = s_pre_flat + p.nmsg * npre;
+    int* s_tb_flat = s_pre_flat + p.nmsg * npre;
     auto s_pre = [&](int m, int i) -> int& { return s_pre_flat[m * npre + i]; };
+    auto s_tb = [&](int m, int i) -> int& { return s_tb_flat[m * p.tiles_per_cta + i]; };
     __shared__ unsigned s_warp[kDecThreads / 32];
     __shared__ unsigned short s_list[kMaxTouched];  // local indices with c != 0 (< 32768)
     __shared__ int s_abort;
@@ -180,9 +211,22 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int t0 = p.tile_begin + blockIdx.x * p.tiles_per_cta;
-    const int nt = min(p.tiles_per_cta, p.tile_end - t0);
-    const long long base = (long long)t0 * kTile;
+    // the CTA's tiles are strided by the grid (slot i holds tile t0 + i * G):
+    // message density varies by parameter segment, and striding spreads the
+    // dense segments' words evenly over the CTAs
+    const int G = (int)gridDim.x;
+    const int t0 = p.tile_begin + (int)blockIdx.x;
+    const int nt = min(p.tiles_per_cta, (p.tile_end - t0 + G - 1) / G);
+    const float inv_g = 1.0f / (float)G;
+    auto tile_of = [&](int i) -> long long { return (long long)t0 + (long long)i * G; };
+    // local count index (slot * kTile + offset) <-> parameter index
+    auto local_of = [&](unsigned idx) -> int {
+        const int slot = __float2int_rn((float)((int)(idx / kTile) - t0) * inv_g);  // exact: a multiple of G
+        return slot * kTile + (int)(idx & (kTile - 1));
+    };
+    auto global_of = [&](int local) -> long long {
+        return tile_of(local / kTile) * kTile + (local & (kTile - 1));
+    };
     const int nq = nt * (kTile / 16);  // int4 chunks of 16 counts
 
     if (tid == 0) s_abort = 0;
@@ -204,7 +248,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         // per (message, tile) counts
         for (int idx = tid; idx < p.nmsg * nt; idx += kDecThreads) {
             const int m = idx / nt, i = idx - m * nt;
-            s_pre(m, i + 1) = seg_count(p, m, t0 + i);
+            s_pre(m, i + 1) = seg_count(p, m, tile_of(i));
         }
         __syncthreads();
         for (int m = tid; m < p.nmsg; m += kDecThreads) {  // exclusive prefix over the CTA's tiles
@@ -213,23 +257,27 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         }
         stamp(2);
     } else {
+        // contiguous messages: each tile's words start at off[m][tile]
+        for (int idx = tid; idx < p.nmsg * nt; idx += kDecThreads) {
+            const int m = idx / nt, i = idx - m * nt;
+            const int b = __ldg(p.off[m] + tile_of(i));
+            s_tb(m, i) = b;
+            s_pre(m, i + 1) = __ldg(p.off[m] + tile_of(i) + 1) - b;
+        }
+        __syncthreads();
         for (int m = tid; m < p.nmsg; m += kDecThreads) {
-            const int b = __ldg(p.off[m] + t0);
-            s_beg[m] = b;
             s_pre(m, 0) = 0;
-            s_pre(m, nt) = __ldg(p.off[m] + t0 + nt) - b;
+            for (int i = 1; i <= nt; ++i) s_pre(m, i) += s_pre(m, i - 1);
         }
     }
     __syncthreads();
 
     // the f-th word of message m among this CTA's words
     auto word_at = [&](int m, int f) -> unsigned {
-        if (SEG) {
-            int i = 0;
-            while (i + 1 < nt && f >= s_pre(m, i + 1)) ++i;
-            return __ldcg(p.seg[m] + (long long)(t0 + i) * kTile + (f - s_pre(m, i)));
-        }
-        return __ldg(p.words[m] + s_beg[m] + f);
+        int i = 0;
+        while (i + 1 < nt && f >= s_pre(m, i + 1)) ++i;
+        if (SEG) return __ldcg(p.seg[m] + tile_of(i) * kTile + (f - s_pre(m, i)));
+        return __ldg(p.words[m] + s_tb(m, i) + (f - s_pre(m, i)));
     };
 
     // words [from, len) of message m into the counts, kBatch independent loads
@@ -246,7 +294,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
 #pragma unroll
             for (int u = 0; u < kBatch; ++u) {
                 if (f0 + u * kDecThreads < len) {
-                    const int local = (int)((w[u] >> 1) - (unsigned)base);
+                    const int local = local_of(w[u] >> 1);
                     s_cnt[local] = (signed char)(s_cnt[local] + ((w[u] & 1u) ? -1 : 1));
                 }
             }
@@ -276,7 +324,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
         for (int u = 0; u < kPre; ++u) {
             if (u * kDecThreads + tid < len) {
                 const unsigned word = pre[m][u];
-                const int local = (int)((word >> 1) - (unsigned)base);
+                const int local = local_of(word >> 1);
                 s_cnt[local] = (signed char)(s_cnt[local] + ((word & 1u) ? -1 : 1));
             }
         }
@@ -293,7 +341,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     if (p.counts_out) {
         for (int q = tid; q < nq; q += kDecThreads) {
             const int4 packed = s_cnt4[q];
-            const long long i0 = base + (long long)q * 16;
+            const long long i0 = global_of(q * 16);
             if (i0 + 16 <= p.n) {
                 reinterpret_cast<int4*>(p.counts_out + i0)[0] = packed;
             } else {
@@ -307,7 +355,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     if constexpr (MODE == GTC_ACCUM_MOMENTUM) {
         // SGD-momentum (M1): dense over the CTA's elements -- every momentum
         // decays -- with 4 float4 of target and of buf in flight per thread
-        dense_momentum(p, reinterpret_cast<const int*>(s_cnt), base, nt);
+        dense_momentum(p, reinterpret_cast<const int*>(s_cnt), t0, G, nt);
         stamp(5);
         return;
     }
@@ -361,11 +409,7 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
             }
         }
         __syncthreads();
-        for (unsigned i = tid; i < total; i += kDecThreads) {
-            const int local = s_list[i];
-            const long long gi = base + local;
-            if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
-        }
+        apply_list<MODE>(p, s_list, s_cnt, total, global_of);
     } else {
         // dense CTA: one list per round u of 256 chunks (4096 counts), each
         // built by a block scan and applied with independent loads; a round
@@ -400,18 +444,14 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
                     s_list[pos++] = (unsigned short)(q * 16 + b);
                 }
                 __syncthreads();
-                for (unsigned i = tid; i < tot; i += kDecThreads) {
-                    const int local = s_list[i];
-                    const long long gi = base + local;
-                    if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
-                }
+                apply_list<MODE>(p, s_list, s_cnt, tot, global_of);
             } else {
                 unsigned msk = msk_u;
                 while (msk) {
                     const int b = __ffs(msk) - 1;
                     msk &= msk - 1;
                     const int local = q * 16 + b;
-                    const long long gi = base + local;
+                    const long long gi = global_of(local);
                     if (gi < p.n) apply_one<MODE>(p, gi, s_cnt[local], p.target[gi]);
                 }
             }
@@ -536,11 +576,11 @@ cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
     auto kern = gtc_decode_apply_kernel<MODE, SEG>;
     static int resident[GTC_MAX_MSGS + 1][kDecMaxTilesPerCta + 1] = {{0}};
     auto dyn_smem = [&](int tpc) {
-        return (size_t)tpc * kTile + sizeof(int) * (size_t)p_in.nmsg * (tpc + 2);
+        return (size_t)tpc * kTile + sizeof(int) * (size_t)p_in.nmsg * (2 * tpc + 1);
     };
     static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    kDecMaxTilesPerCta * kTile + sizeof(int) * GTC_MAX_MSGS *
-                                                   (kDecMaxTilesPerCta + 2));
+                                                   (2 * kDecMaxTilesPerCta + 1));
     if (attr != cudaSuccess) return attr;
     DecodeParams p = p_in;
     const int sms = sm_count();
