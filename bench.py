@@ -276,15 +276,22 @@ def run_gtc(args):
     for t in range(max(3, args.warmup)):
         step(t)
     torch.cuda.synchronize()
+    stepf = ctx.stepper(grads, r, w, args.alpha, amode, stream)
+    # one kernel per gtc_step?  (world 1: the fused encode+apply; world > 1,
+    # p2p: the fused encode+exchange+decode kernel, step_p2p.cu)
+    l0 = ctx.kernel_launches()
+    stepf(0)
+    torch.cuda.synchronize()
+    one_kernel = ctx.kernel_launches() - l0 == 1
 
-    # Timed region: K steps through the one-call C entry point (gtc_step: at
-    # world 1 a single fused kernel; at world > 1 encode + p2p decode).  Every
-    # EV_EVERY-th step is bracketed by CUDA events (same stream): at world 1
-    # that is the fused kernel's duration; at world > 1 those steps run as the
-    # three separate calls with events between them (per-kernel durations).
+    # Timed region: K steps through the one-call C entry point (gtc_step: one
+    # fused kernel at world 1 and, p2p, at world > 1).  Every EV_EVERY-th step
+    # is bracketed by CUDA events (same stream): with one kernel per step that
+    # is the kernel's duration; otherwise (NCCL exchange, momentum at world > 1)
+    # those steps run as the three separate calls with events between them
+    # (per-kernel durations).
     K = args.steps
     EV_EVERY = 8
-    stepf = ctx.stepper(grads, r, w, args.alpha, amode, stream)
     inst = [t for t in range(K) if t % EV_EVERY == 0]
     ev = {t: [torch.cuda.Event(enable_timing=True) for _ in range(4)] for t in inst}
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -300,7 +307,7 @@ def run_gtc(args):
     for t in range(K):
         if t % EV_EVERY == 0:
             e = ev[t]
-            if world == 1:
+            if one_kernel:
                 e[0].record(stream)
                 stepf(t)
                 e[1].record(stream)
@@ -332,12 +339,14 @@ def run_gtc(args):
     ks_local = ctx.last_counts()
     k_rank = ks_local[rank] if world > 1 else ks_local[0]
 
-    # unfused breakdown (world 1; untimed by the step metric): encode kernel
-    # alone and the decode kernel alone, CUDA events on the stream
+    # unfused breakdown (untimed by the step metric): the encode kernel alone
+    # and the exchange + decode alone (separate calls), CUDA events on the stream
     brk = None
-    if world == 1:
+    if one_kernel:
         B = 64
         eb = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(B)]
+        if world > 1:
+            dist.barrier()
         for t in range(B):
             eb[t][0].record(stream)
             ctx.encode(grads[t % NB], r)
@@ -346,8 +355,11 @@ def run_gtc(args):
             ctx.decode_apply(w, args.alpha, amode)
             eb[t][2].record(stream)
         torch.cuda.synchronize()
-        brk = {"encode_only_ms": sum(e[0].elapsed_time(e[1]) for e in eb) / B,
-               "decode_only_ms": sum(e[1].elapsed_time(e[2]) for e in eb) / B}
+        bt = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in eb) / B,
+                           sum(e[1].elapsed_time(e[2]) for e in eb) / B], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(bt, op=dist.ReduceOp.MAX)
+        brk = {"encode_only_ms": bt[0].item(), "decode_only_ms": bt[1].item()}
 
     # density of the touched set (for the decode's algorithmic bytes), untimed
     cnt = torch.empty(n, dtype=torch.int8, device=dev)
@@ -364,8 +376,9 @@ def run_gtc(args):
     ms, enc_ms_max, exch_ms_max, dec_ms_max = stats.tolist()
     ms_per_step = ms / K
     enc_ms_events = enc_ms
-    if world == 1:
-        # world 1: the step IS one kernel (the fused encode); its average
+    if one_kernel:
+        # the step IS one kernel (world 1: the fused encode + apply; world > 1:
+        # the fused encode + exchange + decode + apply); its average
         # launch duration over the timed region, launch gaps included, is the
         # region's event time / K (the bracketing events of the sampled steps
         # stall the stream and would overstate it)
@@ -415,11 +428,20 @@ def run_gtc(args):
     # ---- roofline of the dominant kernel and the decode
     peak, peak_src = measured_peaks()
     ntiles = math.ceil(n / gtc.GTC_TILE)
+    nvl_bytes = 0
     if world == 1:
         # the fused step kernel: stream g, r -> r (12 B/param), words (4 k),
         # tags (8 B/tile), target read-modify-write of the k touched elements
         enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles + (16 * n if momentum else 8 * k_rank)
         kernel_name = "gtc_encode_tile_kernel (fused apply, world 1)"
+    elif one_kernel:
+        # the fused p2p step kernel, local HBM: the encode (12 n + 4 k + 8 T),
+        # this rank's words and tags read back by the decode (4 k + 8 T), the
+        # target read-modify-write of the touched elements (8 nnz); the peers'
+        # words and tags cross NVLink (nvlink_bytes_per_rank)
+        enc_bytes = 12 * n + 8 * k_rank + 16 * ntiles + 8 * nnz_c
+        nvl_bytes = 4 * (sum(k_all) - k_rank) + 8 * (world - 1) * ntiles
+        kernel_name = "gtc_step_p2p_kernel (fused encode + exchange + decode + apply)"
     else:
         enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles
         kernel_name = "gtc_encode_tile_kernel"
@@ -429,7 +451,7 @@ def run_gtc(args):
     # count; momentum: w and buf read and written, 16 B per parameter)
     dec_bytes = 4 * sum_k + 8 * world * ntiles + (16 * n if momentum else 8 * nnz_c)
     dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9 if world > 1 and dec_ms > 0 else None
-    step_bytes = enc_bytes + (dec_bytes + 4 * (world - 1) * max(k_all) if world > 1 else 0)
+    step_bytes = enc_bytes + (dec_bytes + 4 * (world - 1) * max(k_all) if world > 1 and not one_kernel else 0)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "encode_dram_bytes.json")
     if os.path.exists(tpath):
@@ -463,7 +485,8 @@ def run_gtc(args):
                      "alg_bytes_per_launch": enc_bytes, "ms_per_launch": enc_ms,
                      "peak_source": peak_src,
                      "ms_per_launch_sampled_events": enc_ms_events,
-                     "share_of_step": enc_ms / ms_per_step},
+                     "share_of_step": enc_ms / ms_per_step,
+                     "nvlink_bytes_per_rank": nvl_bytes},
         "kernels": {"encode_ms": enc_ms, "exchange_ms": exch_ms, "decode_apply_ms": dec_ms,
                     "unfused_breakdown": brk,
                     "decode_apply_GBs": dec_gbs, "decode_alg_bytes": dec_bytes, "nnz_counts": nnz_c,

@@ -242,6 +242,13 @@ int64_t gtc_kernel_launches(const gtc_ctx* ctx);
  * host memory.  Not for production use. */
 gtc_status gtc_debug_decode_trace(uint64_t* host, int max_entries);
 
+/* Debug: with GTC_DECODE_TRACE=1, the fused p2p step kernel (gtc_step at
+ * world > 1) stamps %globaltimer (ns) at 5 phase boundaries (start, every
+ * rank's tile tag seen, counts done, encode done, end) plus the SM id, 6
+ * entries per CTA for its first 16384 CTAs; this copies up to max_entries of
+ * the last fused step to host memory.  Not for production use. */
+gtc_status gtc_debug_step_trace(uint64_t* host, int max_entries);
+
 const char* gtc_strerror(gtc_status status);
 const char* gtc_last_error_detail(const gtc_ctx* ctx);
 

@@ -65,6 +65,7 @@ _SIGS = {
     "gtc_exchange_mode": (_i32, [_vp]),
     "gtc_kernel_launches": (_i64, [_vp]),
     "gtc_debug_decode_trace": (_i32, [_vp, _i32]),
+    "gtc_debug_step_trace": (_i32, [_vp, _i32]),
     "gtc_strerror": (ctypes.c_char_p, [_i32]),
     "gtc_last_error_detail": (ctypes.c_char_p, [_vp]),
     "gtc_destroy": (None, [_vp]),
@@ -223,6 +224,15 @@ def gtc_debug_decode_trace(max_entries: int = 4096 * 6):
 
     buf = np.zeros(max_entries, dtype=np.uint64)
     _chk(load_library().gtc_debug_decode_trace(buf.ctypes.data_as(_vp), max_entries), "gtc_debug_decode_trace")
+    return buf
+
+
+def gtc_debug_step_trace(max_entries: int = 16384 * 6):
+    """Debug: phase stamps (ns) + SM id per CTA of the last fused p2p step (GTC_DECODE_TRACE=1)."""
+    import numpy as np
+
+    buf = np.zeros(max_entries, dtype=np.uint64)
+    _chk(load_library().gtc_debug_step_trace(buf.ctypes.data_as(_vp), max_entries), "gtc_debug_step_trace")
     return buf
 
 

@@ -34,6 +34,7 @@
 // Algorithmic HBM bytes per launch: 4 * (sum of message words) (read) +
 // 8 * nmsg * num_tiles (tags) + 8 * |{i : c_i != 0}| (target RMW).
 #include "gtc_internal.cuh"
+#include "tile_encode.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -276,7 +277,10 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     auto word_at = [&](int m, int f) -> unsigned {
         int i = 0;
         while (i + 1 < nt && f >= s_pre(m, i + 1)) ++i;
-        if (SEG) return __ldcg(p.seg[m] + tile_of(i) * kTile + (f - s_pre(m, i)));
+        if (SEG) {
+            const unsigned e = __ldcg(p.seg[m] + tile_of(i) * kTile + (f - s_pre(m, i)));
+            return p.stamped ? entry_word(e, tile_of(i)) : e;
+        }
         return __ldg(p.words[m] + s_tb(m, i) + (f - s_pre(m, i)));
     };
 

@@ -36,6 +36,7 @@
 // HBM bytes per parameter (algorithmic): 4 (read g) + 4 (read r) + 4 (write r)
 // + 4*rho (write words); + 8 B per tile (tag).
 #include "gtc_internal.cuh"
+#include "tile_encode.cuh"
 
 #include <cstdlib>
 #include <cstring>
@@ -87,24 +88,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
         :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
-}
-
-__device__ __forceinline__ void st_stream(float4* p, const float4& v) {
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
-                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
-}
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
-__device__ __forceinline__ float comp(const float4& v, int e) {
-    return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
-}
-__device__ __forceinline__ void set_comp(float4& v, int e, float x) {
-    if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
 }
 
 template <bool HAS_G>
@@ -273,29 +256,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const 
     }
 }
 
-// One tile per CTA (the default variant): 256 threads, four 128-bit loads of
-// r and four of g per thread issued before any use, 4 CTAs per SM; no shared
-// state between CTAs.  Same arithmetic and word order as the persistent
-// variant above.
-constexpr int kTileThreads = 256;
-constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kTileVec = kTile / (kTileThreads * 4);  // 4
-static_assert(kTileVec * kTileWarps == 32, "one (round, warp) scan entry per lane");
-
-__device__ __forceinline__ float4 ld_nc_v4(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
-
-__device__ __forceinline__ float4 ld_v4(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
-
 // TMA = true: the tile's r (and g) arrive by two 16 KB 1-D bulk copies into
 // shared memory (one mbarrier), so the loads in flight do not occupy
 // registers and more CTAs fit per SM (GTC_ENCODE_VARIANT=tma).
@@ -311,7 +271,7 @@ __device__ __forceinline__ void momentum_elem(float& w, float& b, int c, float t
 template <int CMP, bool HAS_G, bool TMA, bool MOM>
 __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_kernel(const EncodeParams p) {
     __shared__ unsigned s_scan[kTileVec * kTileWarps];
-    __shared__ unsigned s_total;
+    __shared__ unsigned s_total, s_prev;
     extern __shared__ __align__(128) float4 s_tile[];  // TMA: [r | g] of the tile
     __shared__ __align__(8) unsigned long long s_bar;
 
@@ -346,45 +306,14 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
             rv[j] = s_tile[j * kTileThreads + tid];
             if (HAS_G) gv[j] = s_tile[kVec4PerTile + j * kTileThreads + tid];
         }
-    } else if (full_tile) {
-        const float4* r4 = reinterpret_cast<const float4*>(p.r + base);
-#pragma unroll
-        for (int j = 0; j < kTileVec; ++j) rv[j] = ld_v4(r4 + j * kTileThreads + tid);
-        if (HAS_G) {
-            const float4* g4 = reinterpret_cast<const float4*>(p.g + base);
-#pragma unroll
-            for (int j = 0; j < kTileVec; ++j) gv[j] = ld_nc_v4(g4 + j * kTileThreads + tid);
-        }
     } else {
-#pragma unroll
-        for (int j = 0; j < kTileVec; ++j) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const long long i = base + (long long)(j * kTileThreads + tid) * 4 + e;
-                set_comp(rv[j], e, i < p.n ? p.r[i] : 0.0f);
-                if (HAS_G) set_comp(gv[j], e, i < p.n ? p.g[i] : 0.0f);
-            }
-        }
+        load_tile<HAS_G>(p, base, full_tile, tid, rv, gv);
     }
 
     const float tau = p.tau;
-    unsigned sel = 0u, neg = 0u;
-    bool nonfinite = false;
-#pragma unroll
-    for (int j = 0; j < kTileVec; ++j) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float v = HAS_G ? __fadd_rn(comp(rv[j], e), comp(gv[j], e)) : comp(rv[j], e);
-            const float a = fabsf(v);
-            nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
-            const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
-            const bool ng = v < 0.0f;
-            const float rn = sl ? (ng ? __fadd_rn(v, tau) : __fsub_rn(v, tau)) : v;
-            set_comp(rv[j], e, rn);
-            sel |= (unsigned)sl << (j * 4 + e);
-            neg |= (unsigned)(sl && ng) << (j * 4 + e);
-        }
-    }
+    unsigned sel, neg;
+    bool nonfinite;
+    quantize<CMP, HAS_G>(rv, gv, tau, sel, neg, nonfinite);
 
     // world 1 fused apply (gtc_step): this rank's own quanta are the whole
     // aggregate; load the selected targets now so the latency overlaps the
@@ -410,67 +339,31 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
         late = rem;
     }
 
-    if (full_tile) {
-        float4* r4 = reinterpret_cast<float4*>(p.r + base);
-#pragma unroll
-        for (int j = 0; j < kTileVec; ++j) st_stream(r4 + j * kTileThreads + tid, rv[j]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < kTileVec; ++j) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const long long i = base + (long long)(j * kTileThreads + tid) * 4 + e;
-                if (i < p.n) p.r[i] = comp(rv[j], e);
-            }
-        }
-    }
+    store_residual(p, base, full_tile, tid, rv);
     if (__any_sync(kFull, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
 
-    const unsigned lt = lanemask_lt();
     unsigned my_off[kTileVec];
-#pragma unroll
-    for (int j = 0; j < kTileVec; ++j) {
-        const unsigned c = __popc((sel >> (4 * j)) & 0xfu);  // 0..4
-        const unsigned b0 = __ballot_sync(kFull, c & 1u);
-        const unsigned b1 = __ballot_sync(kFull, c & 2u);
-        const unsigned b2 = __ballot_sync(kFull, c & 4u);
-        my_off[j] = __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
-        if (lane == 0) s_scan[j * kTileWarps + warp] = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
-    }
+    tile_scan_ballots(sel, lane, warp, my_off, s_scan);
     __syncthreads();
     if (warp == 0) {
-        const unsigned x = s_scan[lane];
-        unsigned incl = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-        }
-        s_scan[lane] = incl - x;
+        const unsigned incl = tile_scan_finish(lane, s_scan);
         if (lane == 31) {
             s_total = incl;
-            if (!p.publish_sys) p.tags[tile] = make_tag(p.epoch, incl);
+            // p2p: the count of this slot's previous (same-parity) step, whose
+            // entries beyond the new count are cleared (tile_encode.cuh)
+            if (p.publish_sys) s_prev = (unsigned)(p.tags[tile] & 0xffffffffull);
+            else p.tags[tile] = make_tag(p.epoch, incl);
             if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);    // integer: order-free
             if (tile == 0) *p.k_next = 0ull;
         }
     }
     __syncthreads();
     const unsigned total = s_total;
-    if (total != 0) {
-        unsigned* dst = p.seg + base;
-#pragma unroll
-        for (int j = 0; j < kTileVec; ++j) {
-            unsigned o = s_scan[j * kTileWarps + warp] + my_off[j];
-            const unsigned i0 = (unsigned)(base + (long long)(j * kTileThreads + tid) * 4);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if ((sel >> (4 * j + e)) & 1u) {
-                    dst[o] = ((i0 + e) << 1) | ((neg >> (4 * j + e)) & 1u);
-                    ++o;
-                }
-            }
-        }
-    }
+    if (p.publish_sys)
+        store_words<true>(p.seg + base, base, tid, sel, neg, my_off, s_scan, warp, total, s_prev,
+                          entry_stamp(p.epoch));
+    else
+        store_words<false>(p.seg + base, base, tid, sel, neg, my_off, s_scan, warp, total, 0u, 0u);
     if (MOM) {
         // dense momentum apply over the whole tile: 16 B/param more
         if (full_tile) {
@@ -528,7 +421,7 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
             apply(b, p.target[base + (long long)((b >> 2) * kTileThreads + tid) * 4 + (b & 3)]);
         }
     }
-    if (p.publish_sys && tid == 0) p.tags[tile] = make_tag(p.epoch, total);  // published by gtc_publish_kernel
+    if (p.publish_sys && tid == 0) p.tags[tile] = make_tag(p.epoch, total);  // p2p: after the scan's reads of the old tag
 }
 
 // Kernel 2 (packing, on demand): group sums of kGroupTiles tile counts, one
@@ -615,7 +508,7 @@ __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const Comp
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const unsigned j = j0 + u * 32 + lane;
-            if (j < my_cnt && dst0 + j < p.capacity) p.words[dst0 + j] = w[u];
+            if (j < my_cnt && dst0 + j < p.capacity) p.words[dst0 + j] = p.stamped ? entry_word(w[u], tile) : w[u];
         }
     }
 }
@@ -702,7 +595,7 @@ cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
 
 template <int CMP>
 cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
-    if (use_persistent() && !p.target && p.tile_begin == 0 && p.tile_end == p.num_tiles)
+    if (use_persistent() && !p.target && !p.publish_sys && p.tile_begin == 0 && p.tile_end == p.num_tiles)
         return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
     return p.g ? launch_tile<CMP, true>(p, s) : launch_tile<CMP, false>(p, s);
 }

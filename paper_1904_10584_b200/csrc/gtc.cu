@@ -47,11 +47,14 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 //   recv      u32[world * capacity]              nccl: all-gathered messages
 //   recv_off  i32[world * (T + 1)]               nccl: all-gathered tile offsets
 //   sim_off   i32[max_sim_msgs * (T + 1)]        tile offsets for decode_apply_msgs
+//   push[p][m] T records of kPushRec bytes        p2p: what rank m pushed (fused step), p < 2
 struct Layout {
     int nseg;
     size_t ctrl, group_sum, seg_tags[2], seg_words[2];
     size_t msg_hdr, msg_off, msg_words;
-    size_t ipc, kx_all, recv, recv_off, sim_off, total;
+    size_t ipc, kx_all, recv, recv_off, sim_off;
+    size_t push, push_slot;  // push[p][m] at push + (p * world + m) * push_slot
+    size_t total;
 };
 
 constexpr size_t kIpcRecord = kIpcRecordBytes;
@@ -83,6 +86,11 @@ Layout make_layout(long long n, int world, bool p2p, long long capacity, int max
         L.recv_off = o; o = align_up(o + sizeof(int) * (size_t)world * (size_t)(tiles + 1), 256);
     }
     L.sim_off = o;   o = align_up(o + sizeof(int) * (size_t)std::max(max_sim_msgs, 0) * (size_t)(tiles + 1), 256);
+    L.push = L.push_slot = 0;
+    if (world > 1 && p2p) {
+        L.push_slot = align_up((size_t)kPushRec * T, 256);
+        L.push = o;  o += 2 * (size_t)world * L.push_slot;
+    }
     L.total = o;
     return L;
 }
@@ -122,6 +130,7 @@ struct gtc_ctx {
     cudaEvent_t ev_chunk[kMaxPipe] = {};
     cudaEvent_t ev_join = nullptr;
     int packed_rank = -1;           // whose message the contiguous region holds (-1: stale)
+    bool push_clean[2] = {true, true};  // p2p: the last step of this parity was fused (or none yet)
 
     long long* host_kx = nullptr;  // pinned, 2 * world
     std::vector<long long> last_k;
@@ -206,6 +215,7 @@ gtc_status pack_contiguous(gtc_ctx* c, int rank, cudaStream_t stream) {
     q.hdr = reinterpret_cast<MsgHeader*>(c->ws + c->L.msg_hdr);
     q.capacity = c->capacity;
     q.ctrl = c->ctrl;
+    q.stamped = (c->world > 1 && c->p2p) ? 1 : 0;
     if (c->num_tiles == 0) {
         cudaError_t e = cudaMemsetAsync(c->ws + c->L.msg_hdr, 0, sizeof(MsgHeader), stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + c->L.msg_off, 0, sizeof(int), stream);
@@ -319,9 +329,12 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     // control block, group sums, tags (epoch 0 = never published) and the
     // contiguous header/offsets start at 0
     cudaError_t e = cudaMemset(b, 0, L.seg_tags[0]);
+    // (p2p: the words too -- entry 0 carries stamp 0, never valid; tile_encode.cuh)
+    const size_t seg_words_bytes = sizeof(unsigned) * (size_t)std::max(c->num_tiles, 1) * kTile;
     for (int i = 0; i < L.nseg && e == cudaSuccess; ++i)
-        e = cudaMemset(b + L.seg_tags[i], 0, L.seg_words[i] - L.seg_tags[i]);
+        e = cudaMemset(b + L.seg_tags[i], 0, L.seg_words[i] - L.seg_tags[i] + (L.nseg == 2 ? seg_words_bytes : 0));
     if (e == cudaSuccess) e = cudaMemset(b + L.msg_hdr, 0, L.msg_words - L.msg_hdr);
+    if (e == cudaSuccess && L.push_slot) e = cudaMemset(b + L.push, 0, 2 * (size_t)c->world * L.push_slot);
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: cudaMemset");
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "bind: sync");
@@ -387,6 +400,7 @@ static gtc_status encode_range(gtc_ctx* c, const float* grad, float* residual, c
     p.mu = c->mom_mu;
     p.epoch = c->epoch;
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
+    if (p.publish_sys) c->push_clean[par] = false;  // this parity's push records are not maintained
     p.num_tiles = c->num_tiles;
     p.tile_begin = tb;
     p.tile_end = te;
@@ -515,6 +529,7 @@ static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode,
     if (c->world == 1 || c->p2p) {
         const int par = seg_parity(c);
         p.segmented = 1;
+        p.stamped = (c->world > 1 && c->p2p) ? 1 : 0;
         for (int i = 0; i < c->world; ++i) {
             unsigned char* b = rank_ws(c, i);
             p.seg[i] = reinterpret_cast<const unsigned*>(b + c->L.seg_words[par]);
@@ -612,6 +627,70 @@ static gtc_status step_pipelined(gtc_ctx* c, const float* grad, float* residual,
     return GTC_OK;
 }
 
+// p2p, world > 1: the fused one-kernel step (step_p2p.cu) unless GTC_STEP_FUSED=0.
+static bool fused_step_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_STEP_FUSED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
+                                 int mode, cudaStream_t stream) {
+    begin_step(c);
+    const int par = seg_parity(c);
+    FusedStepParams f{};
+    EncodeParams& p = f.enc;
+    p.g = grad;
+    p.r = residual;
+    p.n = c->n;
+    p.tau = c->tau;
+    p.seg = reinterpret_cast<unsigned*>(c->ws + c->L.seg_words[par]);
+    p.tags = reinterpret_cast<unsigned long long*>(c->ws + c->L.seg_tags[par]);
+    p.ctrl = c->ctrl;
+    p.k_acc = &c->ctrl->k_acc[c->epoch & 1u];
+    p.k_next = &c->ctrl->k_acc[(c->epoch + 1u) & 1u];
+    p.epoch = c->epoch;
+    p.publish_sys = 1;
+    p.num_tiles = c->num_tiles;
+    p.tile_begin = 0;
+    p.tile_end = c->num_tiles;
+    p.step = c->encodes;
+    for (int i = 0; i < c->world; ++i) {
+        unsigned char* b = rank_ws(c, i);
+        f.seg[i] = reinterpret_cast<const unsigned*>(b + c->L.seg_words[par]);
+        f.tags[i] = reinterpret_cast<const unsigned long long*>(b + c->L.seg_tags[par]);
+        f.push_out[i] = nullptr;
+        f.push_in[i] = nullptr;
+        if (i == c->rank) continue;
+        // this rank's records in rank i's push region, and rank i's in ours
+        unsigned char* out = b + c->L.push + ((size_t)par * c->world + c->rank) * c->L.push_slot;
+        if (!c->push_clean[par]) {
+            // the last step of this parity was not fused: our records on the
+            // peers may hold entries of older steps; clear them
+            cudaError_t e = cudaMemsetAsync(out, 0, c->L.push_slot, stream);
+            if (e != cudaSuccess) return cuda_fail(c, e, "step: push region reset");
+        }
+        f.push_out[i] = out;
+        f.push_in[i] = c->ws + c->L.push + ((size_t)par * c->world + i) * c->L.push_slot;
+    }
+    c->push_clean[par] = true;
+    f.rank = c->rank;
+    f.nranks = c->world;
+    f.lag_groups = step_p2p_lag_groups(c->num_tiles);
+    f.target = target;
+    f.alpha = alpha;
+    f.flags = &c->ctrl->flags;
+    f.trace = decode_trace_enabled() ? 1 : 0;
+    cudaError_t e = launch_step_p2p(f, c->cmp_mode, mode, stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "step: fused p2p launch");
+    c->launches += 1;
+    c->stage = Stage::kBound;
+    return GTC_OK;
+}
+
 gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha, int mode,
                     cudaStream_t stream) {
     if (c && c->world == 1) {
@@ -631,6 +710,13 @@ gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* targe
     }
     if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1) {
         const int K = pipeline_chunks(c);
+        if (K == 1 && fused_step_enabled() && c->world <= kFusedMaxRanks && mode != GTC_ACCUM_MOMENTUM) {
+            gtc_status s = check_encode_args(c, grad, residual);
+            if (s == GTC_OK) s = check_apply_args(c, target, mode);
+            if (s != GTC_OK) return s;
+            DeviceGuard g(c->device);
+            return step_fused_p2p(c, grad, residual, target, alpha, mode, stream);
+        }
         if (K > 1) {
             gtc_status s = check_encode_args(c, grad, residual);
             if (s == GTC_OK) s = check_apply_args(c, target, mode);
@@ -818,6 +904,12 @@ gtc_status gtc_debug_decode_trace(uint64_t* host, int max_entries) {
     if (!host || max_entries < 0) return GTC_EINVAL;
     return read_decode_trace(reinterpret_cast<unsigned long long*>(host), max_entries) == cudaSuccess ? GTC_OK
                                                                                                     : GTC_ECUDA;
+}
+
+gtc_status gtc_debug_step_trace(uint64_t* host, int max_entries) {
+    if (!host || max_entries < 0) return GTC_EINVAL;
+    return read_step_trace(reinterpret_cast<unsigned long long*>(host), max_entries) == cudaSuccess ? GTC_OK
+                                                                                                : GTC_ECUDA;
 }
 
 void gtc_destroy(gtc_ctx* c) {

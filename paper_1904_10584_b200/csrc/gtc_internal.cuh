@@ -102,10 +102,12 @@ struct CompactParams {             // segmented (any rank) -> contiguous (local)
     MsgHeader* hdr;
     long long capacity;
     Ctrl* ctrl;                    // local: sticky flags (capacity)
+    int stamped;                   // p2p: seg holds stamped tile-local entries (tile_encode.cuh)
 };
 
 struct DecodeParams {
     int segmented;                 // 1: seg/tags (hot path), 0: words/off (contiguous)
+    int stamped;                   // segmented p2p: stamped tile-local entries (tile_encode.cuh)
     const unsigned int* words[GTC_MAX_MSGS];       // contiguous
     const int* off[GTC_MAX_MSGS];                  // contiguous: [num_tiles + 1] tile offsets
     const unsigned int* seg[GTC_MAX_MSGS];         // segmented (peer pointers in p2p)
@@ -128,6 +130,34 @@ struct DecodeParams {
     unsigned long long* flags;     // this rank's Ctrl::flags
     int tiles_per_cta;             // set by launch_decode_apply
     int trace;                     // GTC_DECODE_TRACE=1: stamp phase times (debug)
+};
+
+// The fused p2p step (step_p2p.cu): one grid of encode CTAs (one tile each,
+// rows a1-a5) interleaved with decode CTAs (kDecGroup tiles each, rows
+// a6-a8), a decode CTA following the encodes of its tiles by lag_groups
+// groups.  Each encode CTA pushes its tile's record -- tag and the first
+// kPushCap entries -- into every peer's push region with one bulk (TMA) copy
+// per peer, so the decoders read every rank's tiles from local memory;
+// entries beyond kPushCap (tiles denser than 1/8) are pulled from the
+// owner's segmented buffer over NVLink.
+constexpr int kFusedMaxRanks = 8;
+constexpr int kDecGroup = 8;
+constexpr int kPushCap = kTile / 8;
+constexpr int kPushRec = 16 + 4 * kPushCap;          // bytes per tile record: {u64 tag, u64 0, u32 entries[kPushCap]}
+struct FusedStepParams {
+    EncodeParams enc;                                  // this rank's encode (stamped entries, no apply)
+    const unsigned* seg[kFusedMaxRanks];               // every rank's words of this step's parity (peers: NVLink)
+    const unsigned long long* tags[kFusedMaxRanks];    // every rank's tags of this step's parity
+    unsigned char* push_out[kFusedMaxRanks];           // this rank's records in peer m's push region (null: self)
+    const unsigned char* push_in[kFusedMaxRanks];      // rank m's records in this rank's push region (null: self)
+    int rank;
+    int nranks;
+    int lag_groups;                                    // decode group = encode group - lag_groups
+    int num_groups;                                    // ceil(num_tiles / kDecGroup) (set by the launcher)
+    float* target;
+    float alpha;
+    unsigned long long* flags;                         // this rank's Ctrl::flags
+    int trace;                                         // GTC_DECODE_TRACE=1: phase stamps (debug)
 };
 
 struct BoundsParams {
@@ -153,6 +183,9 @@ cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
 cudaError_t launch_publish(Ctrl* ctrl, int slot, unsigned long long step, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
+cudaError_t launch_step_p2p(FusedStepParams& p, int cmp_mode, int accum_mode, cudaStream_t s);
+int step_p2p_lag_groups(int num_tiles);
+cudaError_t read_step_trace(unsigned long long* host, int max_entries);
 cudaError_t read_decode_trace(unsigned long long* host, int max_entries);
 bool decode_trace_enabled();
 

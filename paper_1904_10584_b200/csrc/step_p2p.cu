@@ -1,0 +1,458 @@
+// step_p2p.cu -- the whole GTC step for world > 1 (p2p exchange) as ONE kernel:
+// encode (PAPER.md:222 steps 1-4), exchange ("Each worker communicates the
+// sparse update to all other workers and conversely receives all sparse
+// updates"), aggregate and apply ("The received sparse gradient updates are
+// aggregated and weights are updated based on the aggregate").
+//
+// Grid: groups of kDecGroup ENCODE CTAs followed by one DECODE CTA, plus a
+// tail of decode CTAs; kTileThreads threads, 4 CTAs per SM.
+//   encode CTA (tile t): rows a1-a5 exactly as gtc_encode_tile_kernel, writing
+//     stamped tile-local entries (tile_encode.cuh) and the tile's tag
+//     (epoch << 32 | count) as relaxed system-scope stores -- no fence, no
+//     flag -- and PUSHING the tile's record (tag + first kPushCap entries) to
+//     every peer with one bulk (TMA) copy each, fire-and-forget;
+//   decode CTA (group q - lag_groups): rows a6-a8 for kDecGroup tiles of EVERY
+//     rank (itself included).  All its loads go out at once, all local: every
+//     (tile, rank) tag and a speculative first block of every (tile, rank)
+//     record's entries (peers: the records they pushed here; entries beyond
+//     kPushCap are pulled over NVLink).  An entry counts only once its stamp
+//     is this step's (a stale one is re-polled), so no writer-side fence is
+//     needed.  Counts are int8 in
+//     shared memory, accumulated in ordered per-rank passes (indices are unique
+//     within one rank's tile: no two threads of a pass touch one count, no
+//     atomics, deterministic).  Then u = fl(c * tau), WEIGHTS
+//     t = fmaf(alpha, u, t) / UPDATE t = fl(t + u) on the touched elements
+//     (R8), 128-bit read-modify-write of the float4s holding a non-zero count.
+// Why this shape: a CTA slot is held for its whole lifetime, and the encode is
+// bound by the HBM bytes its resident CTAs keep in flight.  Any NVLink round
+// trip a CTA waits for (~3-9 us while the peer's HBM is saturated by its own
+// encode) stretches its lifetime.  Measured alternatives: the
+// decode of tile t - lag inside the CTA encoding tile t, pulling (-35 %) or
+// pushing with plain remote stores (-45 %); decode CTAs pulling from the
+// peers (-40 %).  Bulk copies return the slot as soon as shared memory is
+// read, and the decode CTAs then only wait on local memory.
+//
+// Progress: a decode CTA waits only for tiles encoded by lower-numbered CTAs
+// of each rank (dispatched earlier, in blockIdx order), whose encodes never
+// wait.  A wait longer than 30 s sets kFlagPeer (GTC_EPEER) and the CTA gives
+// up -- an error, never a hang.
+//
+// Buffer reuse: the segmented buffers alternate with the step parity.  A rank
+// overwrites parity p at step e + 2 only after its step e + 1 kernel read
+// every rank's step e + 1 tiles, which each rank writes after its own step e
+// kernel (the one reading parity p) completed (griddepcontrol.wait).
+//
+// Algorithmic bytes per launch (local HBM): the encode's 12 n + 4 k + 8 T,
+// this rank's entries and tags read back (4 k + 8 T), 8 per touched element
+// (target RMW); over NVLink: the peers' entries and tags, 4 (K - k) + 8 (N-1) T.
+#include "gtc_internal.cuh"
+#include "tile_encode.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+namespace gtc {
+namespace {
+
+constexpr int kSpecPerThread = 4;   // speculative entry loads per thread (decode CTA)
+constexpr int kWordBatch = 4;       // further entry loads per thread before their count updates
+constexpr int kApplyBatch = 4;      // target float4 loads per thread before their stores
+constexpr unsigned long long kTimeoutNs = 30ull * 1000 * 1000 * 1000;
+static_assert(kDecGroup * kFusedMaxRanks <= kTileThreads, "one tag poller per (tile, rank)");
+
+// Opt-in phase trace (GTC_DECODE_TRACE=1): thread 0 of each of the first
+// kStepTraceCtas CTAs stamps %globaltimer at: start, tags seen (decode),
+// counts done (decode), -, end; and (SM id | decode << 16).
+constexpr int kStepTraceCtas = 16384;
+constexpr int kStepTracePhases = 6;
+__device__ unsigned long long g_step_trace[kStepTraceCtas * kStepTracePhases];
+
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* a) {
+    unsigned v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int MODE>
+__device__ __forceinline__ float apply_count(float t, int c, float tau, float alpha) {
+    const float u = __fmul_rn((float)c, tau);
+    return (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(alpha, u, t) : __fadd_rn(t, u);
+}
+
+// Re-poll an entry until it carries `stamp`; false on timeout.
+__device__ __noinline__ bool await_entry(const unsigned* a, unsigned stamp, unsigned& e) {
+    const unsigned long long t0 = now_ns();
+    do {
+        if (now_ns() - t0 > kTimeoutNs) return false;
+        __nanosleep(32);
+        e = ld_relaxed_sys(a);
+    } while ((e >> kStampShift) != stamp);
+    return true;
+}
+
+__device__ __forceinline__ void count_entry(signed char* cnt, unsigned e) {
+    signed char& c = cnt[(e >> 1) & (kTile - 1)];
+    c = (signed char)(c + ((e & 1u) ? -1 : 1));
+}
+
+// ------------------------------------------------------------ encode CTA
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// The encode of tile t (rows a1-a5) as gtc_encode_tile_kernel, plus the push:
+// the tile's record {tag, 0, entries [0, min(count, kPushCap))} is staged in
+// shared memory and sent to every peer with one bulk copy each.  The CTA waits
+// only until the copies have READ shared memory; the NVLink writes complete
+// after it has exited, so no encode slot is held for an NVLink round trip.
+// The copied range also covers the previous same-parity count, zero-filled,
+// which keeps the records' stale-entry invariant (tile_encode.cuh).
+template <int CMP, bool HAS_G>
+__device__ __forceinline__ void encode_cta(const FusedStepParams& f, long long t, unsigned* s_scan, unsigned* s_misc,
+                                           unsigned long long* s_rec) {
+    const EncodeParams& p = f.enc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long base = t * kTile;
+    const bool full_tile = base + kTile <= p.n;
+    float4 rv[kTileVec], gv[kTileVec];
+    load_tile<HAS_G>(p, base, full_tile, tid, rv, gv);
+    unsigned sel, neg;
+    bool nonfinite;
+    quantize<CMP, HAS_G>(rv, gv, p.tau, sel, neg, nonfinite);
+    store_residual(p, base, full_tile, tid, rv);
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
+    unsigned my_off[kTileVec];
+    tile_scan_ballots(sel, lane, warp, my_off, s_scan);
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned incl = tile_scan_finish(lane, s_scan);
+        if (lane == 31) {
+            s_misc[0] = incl;
+            s_misc[1] = (unsigned)(p.tags[t] & 0xffffffffull);  // this slot's previous same-parity count
+            if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);
+            if (t == 0) *p.k_next = 0ull;
+        }
+    }
+    __syncthreads();
+    const unsigned total = s_misc[0], prev = s_misc[1];
+    const unsigned stamp = entry_stamp(p.epoch);
+    unsigned* dst = p.seg + base;
+    unsigned* s_ent = reinterpret_cast<unsigned*>(s_rec + 2);
+    if (total != 0) {
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+            unsigned o = s_scan[j * kTileWarps + warp] + my_off[j];
+            const unsigned l0 = (unsigned)(j * kTileThreads + tid) * 4u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if ((sel >> (4 * j + e)) & 1u) {
+                    const unsigned w = make_entry(stamp, l0 + e, (neg >> (4 * j + e)) & 1u);
+                    st_relaxed_sys(dst + o, w);
+                    if (o < (unsigned)kPushCap) s_ent[o] = w;
+                    ++o;
+                }
+            }
+        }
+    }
+    for (unsigned o = total + tid; o < prev; o += kTileThreads) st_relaxed_sys(dst + o, 0u);
+    const unsigned clr = min(max(total, prev), (unsigned)kPushCap);
+    const unsigned clr4 = (clr + 3u) & ~3u;  // bulk copies move multiples of 16 bytes
+    for (unsigned o = total + tid; o < clr4; o += kTileThreads) s_ent[o] = 0u;
+    const unsigned long long tag = make_tag(p.epoch, total);
+    if (tid == 0) {
+        st_relaxed_sys(p.tags + t, tag);
+        s_rec[0] = tag;
+        s_rec[1] = 0ull;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> the bulk copies
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned bytes = 16u + 4u * clr4;
+#pragma unroll
+        for (int m = 0; m < kFusedMaxRanks; ++m) {
+            if (m >= f.nranks || !f.push_out[m]) continue;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         :: "l"(f.push_out[m] + t * kPushRec), "r"(smem_u32(s_rec)), "r"(bytes) : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+}
+
+// ------------------------------------------------------------ decode CTA
+// Tiles [t0, t0 + ng) of every rank.  A peer timeout sets kFlagPeer.
+template <int MODE, typename Stamp>
+__device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t0, int ng, signed char* s_cnt,
+                                           int* s_k, int* s_abort, const Stamp& stamp_ph) {
+    const EncodeParams& p = f.enc;
+    const int tid = threadIdx.x;
+    const int N = f.nranks;
+    const int SP = kSpecPerThread * kTileThreads / (kDecGroup * N);  // speculative entries per (tile, rank)
+
+    // all loads in flight at once: tags, then the speculative entries
+    // (flat index (i, m, j), j fastest: coalesced per (tile, rank) slot)
+    // rank m's tag and entry j of tile t: peers from this rank's push region
+    // (entries beyond kPushCap from the owner's buffer, over NVLink), this
+    // rank from its own segmented buffer
+    auto tag_ptr = [&](int m, long long t) -> const unsigned long long* {
+        return f.push_in[m] ? reinterpret_cast<const unsigned long long*>(f.push_in[m] + t * kPushRec) : f.tags[m] + t;
+    };
+    auto entry_ptr = [&](int m, long long t, int j) -> const unsigned* {
+        if (f.push_in[m] && j < kPushCap) return reinterpret_cast<const unsigned*>(f.push_in[m] + t * kPushRec + 16) + j;
+        return f.seg[m] + t * kTile + j;
+    };
+    unsigned long long tagv = 0;
+    const int ti = tid / N, tm = tid - ti * N;
+    if (ti < ng) tagv = ld_relaxed_sys(tag_ptr(tm, t0 + ti));
+    unsigned spec[kSpecPerThread];
+    int sm_[kSpecPerThread], si_[kSpecPerThread], sj_[kSpecPerThread];
+#pragma unroll
+    for (int u = 0; u < kSpecPerThread; ++u) {
+        const int fl = tid + u * kTileThreads;
+        si_[u] = fl / (N * SP);
+        sm_[u] = (fl / SP) % N;
+        sj_[u] = fl % SP;
+        spec[u] = 0u;
+        if (si_[u] < ng) spec[u] = ld_relaxed_sys(entry_ptr(sm_[u], t0 + si_[u], sj_[u]));
+    }
+    int4* c4 = reinterpret_cast<int4*>(s_cnt);
+    for (int q = tid; q < kDecGroup * kTile / 16; q += kTileThreads) c4[q] = make_int4(0, 0, 0, 0);
+    if (tid == 0) *s_abort = 0;
+    __syncthreads();
+    if (ti < ng) {
+        if ((unsigned)(tagv >> 32) != p.epoch) {
+            const unsigned long long t0ns = now_ns();
+            do {
+                if (now_ns() - t0ns > kTimeoutNs) {
+                    *s_abort = 1;
+                    break;
+                }
+                __nanosleep(32);
+                tagv = ld_relaxed_sys(tag_ptr(tm, t0 + ti));
+            } while ((unsigned)(tagv >> 32) != p.epoch);
+        }
+        s_k[ti * kFusedMaxRanks + tm] = (int)(tagv & 0xffffffffull);
+    }
+    __syncthreads();
+    stamp_ph(1);
+    if (*s_abort) {
+        if (tid == 0) atomicOr(f.flags, kFlagPeer);
+        return;
+    }
+
+    // ordered per-rank passes
+    const unsigned stamp = entry_stamp(p.epoch);
+    bool ok = true;
+    for (int m = 0; m < N; ++m) {
+#pragma unroll
+        for (int u = 0; u < kSpecPerThread; ++u) {
+            if (!ok || sm_[u] != m || si_[u] >= ng || sj_[u] >= s_k[si_[u] * kFusedMaxRanks + m]) continue;
+            unsigned e = spec[u];
+            if ((e >> kStampShift) != stamp && !await_entry(entry_ptr(m, t0 + si_[u], sj_[u]), stamp, e)) {
+                ok = false;
+                continue;
+            }
+            count_entry(s_cnt + si_[u] * kTile, e);
+        }
+        // entries beyond the speculative block (dense tiles)
+        for (int i = 0; i < ng && ok; ++i) {
+            const int k = s_k[i * kFusedMaxRanks + m];
+            for (int j0 = SP + tid; j0 < k && ok; j0 += kWordBatch * kTileThreads) {
+                unsigned e[kWordBatch];
+#pragma unroll
+                for (int u = 0; u < kWordBatch; ++u)
+                    if (j0 + u * kTileThreads < k) e[u] = ld_relaxed_sys(entry_ptr(m, t0 + i, j0 + u * kTileThreads));
+#pragma unroll
+                for (int u = 0; u < kWordBatch; ++u) {
+                    const int j = j0 + u * kTileThreads;
+                    if (j >= k || !ok) continue;
+                    if ((e[u] >> kStampShift) != stamp && !await_entry(entry_ptr(m, t0 + i, j), stamp, e[u])) {
+                        ok = false;
+                        continue;
+                    }
+                    count_entry(s_cnt + i * kTile, e[u]);
+                }
+            }
+        }
+        if (!ok) *s_abort = 1;
+        __syncthreads();  // the next rank's pass may touch the same counts
+    }
+    stamp_ph(2);
+    if (*s_abort) {
+        if (tid == 0) atomicOr(f.flags, kFlagPeer);
+        return;
+    }
+
+    // apply: thread tid owns elements [16 tid, 16 tid + 16) of each tile, as
+    // four float4 (bit i * 4 + h of `todo`: float4 h of tile i is touched)
+    unsigned todo = 0u;
+    for (int i = 0; i < ng; ++i) {
+        const int4 c = c4[i * (kTile / 16) + tid];
+        const unsigned x[4] = {(unsigned)c.x, (unsigned)c.y, (unsigned)c.z, (unsigned)c.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) todo |= (x[h] != 0u ? 1u : 0u) << (i * 4 + h);
+    }
+    while (todo) {
+        int bit[kApplyBatch];
+        float4 tv[kApplyBatch];
+#pragma unroll
+        for (int u = 0; u < kApplyBatch; ++u) {
+            bit[u] = -1;
+            if (todo) {
+                bit[u] = __ffs(todo) - 1;
+                todo &= todo - 1u;
+                const long long i0 = (t0 + (bit[u] >> 2)) * kTile + 16 * tid + 4 * (bit[u] & 3);
+                if (i0 + 4 <= p.n) tv[u] = *reinterpret_cast<const float4*>(f.target + i0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kApplyBatch; ++u) {
+            if (bit[u] < 0) continue;
+            const int i = bit[u] >> 2, h = bit[u] & 3;
+            const long long i0 = (t0 + i) * kTile + 16 * tid + 4 * h;
+            const int packed = reinterpret_cast<const int*>(s_cnt + i * kTile)[4 * tid + h];
+            const int cc[4] = {(int)(signed char)(packed & 0xff), (int)(signed char)((packed >> 8) & 0xff),
+                               (int)(signed char)((packed >> 16) & 0xff), (int)(signed char)((unsigned)packed >> 24)};
+            if (i0 + 4 <= p.n) {
+                float4 t = tv[u];
+                if (cc[0]) t.x = apply_count<MODE>(t.x, cc[0], p.tau, f.alpha);
+                if (cc[1]) t.y = apply_count<MODE>(t.y, cc[1], p.tau, f.alpha);
+                if (cc[2]) t.z = apply_count<MODE>(t.z, cc[2], p.tau, f.alpha);
+                if (cc[3]) t.w = apply_count<MODE>(t.w, cc[3], p.tau, f.alpha);
+                *reinterpret_cast<float4*>(f.target + i0) = t;
+            } else {
+                for (int e = 0; e < 4 && i0 + e < p.n; ++e)
+                    if (cc[e]) f.target[i0 + e] = apply_count<MODE>(f.target[i0 + e], cc[e], p.tau, f.alpha);
+            }
+        }
+    }
+}
+
+template <int CMP, bool HAS_G, int MODE>
+__global__ void __launch_bounds__(kTileThreads, 4) gtc_step_p2p_kernel(const FusedStepParams f) {
+    __shared__ unsigned s_scan[kTileVec * kTileWarps];
+    __shared__ unsigned s_misc[2];
+    __shared__ int4 s_cnt4[kDecGroup * kTile / 16];  // int8 counts of the decode CTA's tiles
+    __shared__ int s_k[kDecGroup * kFusedMaxRanks];
+    __shared__ int s_abort;
+    __shared__ __align__(128) unsigned long long s_rec[kPushRec / 8];  // the encode's push record
+
+    const EncodeParams& p = f.enc;
+    const long long b = blockIdx.x;
+    const bool trace = f.trace && threadIdx.x == 0 && b < kStepTraceCtas;
+    auto stamp_ph = [&](int ph) {
+        if (trace) g_step_trace[b * kStepTracePhases + ph] = now_ns();
+    };
+
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    stamp_ph(0);
+
+    // CTA role: b < Q * (G + 1): group q = b / (G + 1), slot r = b % (G + 1);
+    // r < G encodes tile q * G + r, r == G decodes group q - lag_groups; the
+    // tail decodes the last min(lag_groups, Q) groups.
+    const long long Q = f.num_groups;
+    long long enc_tile = -1, dec_group = -1;
+    if (b < Q * (kDecGroup + 1)) {
+        const long long q = b / (kDecGroup + 1), r = b - q * (kDecGroup + 1);
+        if (r < kDecGroup) enc_tile = q * kDecGroup + r;
+        else dec_group = q - f.lag_groups;
+    } else {
+        dec_group = (Q - min((long long)f.lag_groups, Q)) + (b - Q * (kDecGroup + 1));
+    }
+    if (trace) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_step_trace[b * kStepTracePhases + 5] = smid | (enc_tile < 0 ? 1u << 16 : 0u);
+    }
+    if (enc_tile >= 0) {
+        if (enc_tile < p.num_tiles) encode_cta<CMP, HAS_G>(f, enc_tile, s_scan, s_misc, s_rec);
+    } else if (dec_group >= 0) {
+        const long long t0 = dec_group * kDecGroup;
+        const int ng = (int)min((long long)kDecGroup, (long long)p.num_tiles - t0);
+        decode_cta<MODE>(f, t0, ng, reinterpret_cast<signed char*>(s_cnt4), s_k, &s_abort, stamp_ph);
+    }
+    stamp_ph(4);
+}
+
+bool pdl_wanted() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <int CMP, bool HAS_G, int MODE>
+cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    const long long Q = f.num_groups;
+    cfg.gridDim = dim3((unsigned)(Q * (kDecGroup + 1) + std::min<long long>(f.lag_groups, Q)));
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_wanted() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gtc_step_p2p_kernel<CMP, HAS_G, MODE>, f);
+}
+
+template <int CMP, bool HAS_G>
+cudaError_t launch_g(FusedStepParams& f, int mode, cudaStream_t s) {
+    return mode == GTC_ACCUM_UPDATE ? launch_t<CMP, HAS_G, GTC_ACCUM_UPDATE>(f, s)
+                                    : launch_t<CMP, HAS_G, GTC_ACCUM_WEIGHTS>(f, s);
+}
+
+}  // namespace
+
+// Decode lag in groups: about one wave of resident CTAs (GTC_FUSED_LAG, in
+// tiles, overrides).
+int step_p2p_lag_groups(int num_tiles) {
+    static std::once_flag once;
+    static int wave = 592;
+    std::call_once(once, [] {
+        int dev = 0, sms = 0, per_sm = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, gtc_step_p2p_kernel<GTC_CMP_GT, true, GTC_ACCUM_WEIGHTS>, kTileThreads, 0) == cudaSuccess &&
+            sms > 0 && per_sm > 0)
+            wave = sms * per_sm;
+        const char* e = std::getenv("GTC_FUSED_LAG");
+        if (e && std::atoi(e) > 0) wave = std::atoi(e);
+    });
+    const int groups = (num_tiles + kDecGroup - 1) / kDecGroup;
+    const int lag = (wave + kDecGroup) / (kDecGroup + 1);  // groups of G + 1 CTAs per wave
+    return std::max(1, std::min(lag, groups));
+}
+
+cudaError_t read_step_trace(unsigned long long* host, int max_entries) {
+    const int n = max_entries < kStepTraceCtas * kStepTracePhases ? max_entries : kStepTraceCtas * kStepTracePhases;
+    return cudaMemcpyFromSymbol(host, g_step_trace, sizeof(unsigned long long) * n);
+}
+
+cudaError_t launch_step_p2p(FusedStepParams& f, int cmp_mode, int accum_mode, cudaStream_t s) {
+    if (f.enc.num_tiles == 0) return cudaSuccess;
+    f.num_groups = (f.enc.num_tiles + kDecGroup - 1) / kDecGroup;
+    if (f.lag_groups < 1) f.lag_groups = 1;
+    if (cmp_mode == GTC_CMP_GE)
+        return f.enc.g ? launch_g<GTC_CMP_GE, true>(f, accum_mode, s) : launch_g<GTC_CMP_GE, false>(f, accum_mode, s);
+    return f.enc.g ? launch_g<GTC_CMP_GT, true>(f, accum_mode, s) : launch_g<GTC_CMP_GT, false>(f, accum_mode, s);
+}
+
+}  // namespace gtc

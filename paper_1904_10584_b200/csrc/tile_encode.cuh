@@ -1,0 +1,218 @@
+// tile_encode.cuh -- device helpers for encoding one tile of kTile params with
+// one CTA of kTileThreads threads (Sec. VI-A; R1-R4).
+// Used by gtc_encode_tile_kernel (encode.cu) and by the fused p2p step kernel
+// (step_p2p.cu).  Not installed.
+//
+// Element order inside a tile: thread `tid` holds float4 j (j < kTileVec) at
+// element offset (j * kTileThreads + tid) * 4, so (round j, warp, lane,
+// component) is ascending index; bit j*4+e of the thread's `sel`/`neg` masks
+// is component e of its float4 j.
+#pragma once
+
+#include "gtc_internal.cuh"
+
+namespace gtc {
+
+constexpr int kTileThreads = 256;
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kTileVec = kTile / (kTileThreads * 4);  // 4
+static_assert(kTileVec * kTileWarps == 32, "one (round, warp) scan entry per lane");
+
+// ---------------------------------------------------------------- p2p entries
+// In p2p mode a rank's segmented message is read by its peers while it may
+// still be being written (the fused step reads tile t of every rank one wave
+// after it was encoded, with no fence on the writer's side).  Every 32-bit
+// entry of a tile slot therefore carries the step that wrote it:
+//     entry = stamp(epoch) << 13 | local << 1 | neg,   local = index - tile * kTile (< 4096)
+// A reader accepts an entry only if its stamp is this step's.  The encoder
+// also clears (entry 0, stamp 0 = never valid) the slots its previous count of
+// the same parity used beyond its new count, so every slot holds either the
+// previous same-parity step's entry or 0, and stamp(e) != stamp(e - 2).
+constexpr int kStampShift = 13;
+static_assert(kTile == 1 << (kStampShift - 1), "local index + sign fill the low 13 bits");
+__host__ __device__ __forceinline__ unsigned entry_stamp(unsigned epoch) { return epoch % 524287u + 1u; }
+__host__ __device__ __forceinline__ unsigned make_entry(unsigned stamp, unsigned local, unsigned neg) {
+    return (stamp << kStampShift) | (local << 1) | neg;
+}
+// the canonical word (index << 1 | neg) of entry `e` of tile `tile`
+__host__ __device__ __forceinline__ unsigned entry_word(unsigned e, long long tile) {
+    return ((unsigned)(tile * kTile) + ((e >> 1) & (kTile - 1))) << 1 | (e & 1u);
+}
+
+__device__ __forceinline__ float4 ld_nc_v4(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ float4 ld_v4(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void st_stream(float4* p, const float4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ float comp(const float4& v, int e) {
+    return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void set_comp(float4& v, int e, float x) {
+    if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
+}
+
+// r (and g) of the tile into registers: 128-bit loads issued before any use
+// (the ragged last tile element by element, zero-padded).
+template <bool HAS_G>
+__device__ __forceinline__ void load_tile(const EncodeParams& p, long long base, bool full_tile, int tid,
+                                          float4 (&rv)[kTileVec], float4 (&gv)[kTileVec]) {
+    if (full_tile) {
+        const float4* r4 = reinterpret_cast<const float4*>(p.r + base);
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) rv[j] = ld_v4(r4 + j * kTileThreads + tid);
+        if (HAS_G) {
+            const float4* g4 = reinterpret_cast<const float4*>(p.g + base);
+#pragma unroll
+            for (int j = 0; j < kTileVec; ++j) gv[j] = ld_nc_v4(g4 + j * kTileThreads + tid);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const long long i = base + (long long)(j * kTileThreads + tid) * 4 + e;
+                set_comp(rv[j], e, i < p.n ? p.r[i] : 0.0f);
+                if (HAS_G) set_comp(gv[j], e, i < p.n ? p.g[i] : 0.0f);
+            }
+        }
+    }
+}
+
+// Rows a1-a3 on the thread's 16 elements: v = fl(r + g); sel = |v| > tau (GT)
+// or >= tau (GE); r = sel ? fl(v -+ tau) : v.  rv holds the new residual.
+template <int CMP, bool HAS_G>
+__device__ __forceinline__ void quantize(float4 (&rv)[kTileVec], const float4 (&gv)[kTileVec], float tau,
+                                         unsigned& sel, unsigned& neg, bool& nonfinite) {
+    sel = 0u;
+    neg = 0u;
+    nonfinite = false;
+#pragma unroll
+    for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float v = HAS_G ? __fadd_rn(comp(rv[j], e), comp(gv[j], e)) : comp(rv[j], e);
+            const float a = fabsf(v);
+            nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
+            const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
+            const bool ng = v < 0.0f;
+            const float rn = sl ? (ng ? __fadd_rn(v, tau) : __fsub_rn(v, tau)) : v;
+            set_comp(rv[j], e, rn);
+            sel |= (unsigned)sl << (j * 4 + e);
+            neg |= (unsigned)(sl && ng) << (j * 4 + e);
+        }
+    }
+}
+
+__device__ __forceinline__ void store_residual(const EncodeParams& p, long long base, bool full_tile, int tid,
+                                               const float4 (&rv)[kTileVec]) {
+    if (full_tile) {
+        float4* r4 = reinterpret_cast<float4*>(p.r + base);
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) st_stream(r4 + j * kTileThreads + tid, rv[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const long long i = base + (long long)(j * kTileThreads + tid) * 4 + e;
+                if (i < p.n) p.r[i] = comp(rv[j], e);
+            }
+        }
+    }
+}
+
+// Row a5, first half: the thread's offsets of its selected elements among
+// the tile's (my_off[j] = words before its float4 j within round j, warp),
+// per (round, warp) totals into s_scan (then exclusive-scanned by warp 0 in
+// tile_scan_finish).
+__device__ __forceinline__ void tile_scan_ballots(unsigned sel, int lane, int warp, unsigned (&my_off)[kTileVec],
+                                                  unsigned* s_scan) {
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < kTileVec; ++j) {
+        const unsigned c = __popc((sel >> (4 * j)) & 0xfu);  // 0..4
+        const unsigned b0 = __ballot_sync(0xffffffffu, c & 1u);
+        const unsigned b1 = __ballot_sync(0xffffffffu, c & 2u);
+        const unsigned b2 = __ballot_sync(0xffffffffu, c & 4u);
+        my_off[j] = __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+        if (lane == 0) s_scan[j * kTileWarps + warp] = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+    }
+}
+
+// Warp 0: exclusive scan of the 32 (round, warp) totals; returns the tile's
+// word count on every lane.
+__device__ __forceinline__ unsigned tile_scan_finish(int lane, unsigned* s_scan) {
+    const unsigned x = s_scan[lane];
+    unsigned incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    s_scan[lane] = incl - x;
+    return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+__device__ __forceinline__ void st_relaxed_sys(unsigned* a, unsigned v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(a), "l"(v) : "memory");
+}
+
+// Rows a4-a5, second half: the thread's words, compacted in ascending index
+// order, into the tile's slot.  STAMPED (p2p): stamped tile-local entries,
+// and the slots [total, prev_total) of the previous same-parity step cleared;
+// RELAXED: as relaxed system-scope stores (peers read them while this kernel
+// runs, the fused step).
+template <bool STAMPED, bool RELAXED = false>
+__device__ __forceinline__ void store_words(unsigned* dst, long long base, int tid, unsigned sel, unsigned neg,
+                                            const unsigned (&my_off)[kTileVec], const unsigned* s_scan, int warp,
+                                            unsigned total, unsigned prev_total, unsigned stamp) {
+    if (total != 0) {
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+            unsigned o = s_scan[j * kTileWarps + warp] + my_off[j];
+            const unsigned l0 = (unsigned)(j * kTileThreads + tid) * 4u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if ((sel >> (4 * j + e)) & 1u) {
+                    const unsigned ng = (neg >> (4 * j + e)) & 1u;
+                    const unsigned w = STAMPED ? make_entry(stamp, l0 + e, ng) : (((unsigned)base + l0 + e) << 1) | ng;
+                    if (RELAXED) st_relaxed_sys(dst + o, w);
+                    else dst[o] = w;
+                    ++o;
+                }
+            }
+        }
+    }
+    if (STAMPED) {
+        for (unsigned o = total + tid; o < prev_total; o += kTileThreads) {
+            if (RELAXED) st_relaxed_sys(dst + o, 0u);
+            else dst[o] = 0u;
+        }
+    }
+}
+
+}  // namespace gtc

@@ -28,9 +28,10 @@ def main():
     steps = int(os.environ.get("GTC_STEPS", 4))
     cmp = os.environ.get("GTC_CMP", "gt")
     exchange = os.environ.get("GTC_EXCHANGE", "p2p")
-    momentum = os.environ.get("GTC_ACCUM", "weights") == "momentum"
-    gmode = gtc.GTC_ACCUM_MOMENTUM if momentum else gtc.GTC_ACCUM_WEIGHTS
-    omode = oracle.ACCUM_MOMENTUM if momentum else oracle.ACCUM_WEIGHTS
+    accum = os.environ.get("GTC_ACCUM", "weights")
+    momentum = accum == "momentum"
+    gmode = {"weights": gtc.GTC_ACCUM_WEIGHTS, "update": gtc.GTC_ACCUM_UPDATE, "momentum": gtc.GTC_ACCUM_MOMENTUM}[accum]
+    omode = {"weights": oracle.ACCUM_WEIGHTS, "update": oracle.ACCUM_UPDATE, "momentum": oracle.ACCUM_MOMENTUM}[accum]
     mu = 0.9
     tau = 8.0
     torch.cuda.set_device(local)
@@ -77,14 +78,23 @@ def main():
         hs = [None] * world
         dist.all_gather_object(hs, h)
         assert len(set(hs)) == 1, f"replicas differ at step {t}"
-    # the one-call step (p2p: pipelined encode/decode chunks on two streams)
+    # the one-call step (p2p: one fused encode+exchange+decode kernel, or the
+    # pipelined chunks with GTC_PIPELINE_CHUNKS > 1); odd steps start the ranks
+    # at different times so the in-kernel waits on peers' tiles are exercised
     for t in range(steps, 2 * steps):
         gs = [synth.correlated_gradient(n, 4.0, synth.BASE_SEED, t, w) for w in range(world)]
-        st = ctx.step(torch.from_numpy(gs[rank]).to(dev), rd, wd, -0.5, gmode)
+        g_dev = torch.from_numpy(gs[rank]).to(dev)
+        if t % 2 == 1:
+            torch.cuda._sleep(int(1e6 * ((rank + t) % world)))
+        st = ctx.step(g_dev, rd, wd, -0.5, gmode)
         assert st == gtc.GTC_OK, st
         torch.cuda.synchronize()
-        oracle.step(gs, r_or, w_or, tau, mode, -0.5, omode, buf=buf_or, mu=mu)
+        assert ctx.check() == gtc.GTC_OK
+        om, _, _ = oracle.step(gs, r_or, w_or, tau, mode, -0.5, omode, buf=buf_or, mu=mu)
         check_buf(f"rank {rank} step {t}: momentum buffer (gtc_step)")
+        assert ctx.last_counts() == [m.size for m in om], (ctx.last_counts(), [m.size for m in om])
+        for w in range(world):
+            assert np.array_equal(ctx.read_message(w), om[w]), f"rank {rank} step {t}: message of rank {w} (gtc_step)"
         assert np.array_equal(rd.cpu().numpy().view(np.uint32), r_or[rank].view(np.uint32)), f"step {t}: residual"
         wh = wd.cpu().numpy()
         assert np.array_equal(wh.view(np.uint32), w_or.view(np.uint32)), f"step {t}: weights (gtc_step)"

@@ -82,3 +82,32 @@ def test_pipelined_step_parity():
            "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("world,lag,accum", [(2, "1", "weights"), (2, "7", "update"), (3, "64", "weights"),
+                                             (4, "5", "weights"), (4, "0", "update")])
+def test_fused_step_parity(world, lag, accum):
+    """The fused one-kernel p2p step (step_p2p.cu) with short decode lags, so
+    CTAs wait on peers' tiles still being written (stamped entries), and with
+    the default lag ("0"); ranks start skewed on odd steps."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="4", GTC_N="1000003", GTC_EXCHANGE="p2p", GTC_ACCUM=accum)
+    if lag != "0":
+        env["GTC_FUSED_LAG"] = lag
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29536", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MULTIGPU OK" in p.stdout
+
+
+def test_unfused_step_parity():
+    """gtc_step as separate encode / decode kernels (GTC_STEP_FUSED=0)."""
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    env = dict(os.environ, GTC_CMP="ge", GTC_STEPS="4", GTC_N="1000003", GTC_EXCHANGE="p2p", GTC_STEP_FUSED="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
