@@ -56,7 +56,6 @@ namespace gtc {
 namespace {
 
 constexpr int kSpecPerThread = 4;   // speculative entry loads per thread (decode CTA)
-constexpr int kWordBatch = 4;       // further entry loads per thread before their count updates
 constexpr int kApplyBatch = 4;      // target float4 loads per thread before their stores
 constexpr unsigned long long kTimeoutNs = 30ull * 1000 * 1000 * 1000;
 static_assert(kDecGroup * kFusedMaxRanks <= kTileThreads, "one tag poller per (tile, rank)");
@@ -90,17 +89,6 @@ template <int MODE>
 __device__ __forceinline__ float apply_count(float t, int c, float tau, float alpha) {
     const float u = __fmul_rn((float)c, tau);
     return (MODE == GTC_ACCUM_WEIGHTS) ? __fmaf_rn(alpha, u, t) : __fadd_rn(t, u);
-}
-
-// Re-poll an entry until it carries `stamp`; false on timeout.
-__device__ __noinline__ bool await_entry(const unsigned* a, unsigned stamp, unsigned& e) {
-    const unsigned long long t0 = now_ns();
-    do {
-        if (now_ns() - t0 > kTimeoutNs) return false;
-        __nanosleep(32);
-        e = ld_relaxed_sys(a);
-    } while ((e >> kStampShift) != stamp);
-    return true;
 }
 
 __device__ __forceinline__ void count_entry(signed char* cnt, unsigned e) {
@@ -217,16 +205,21 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
     unsigned long long tagv = 0;
     const int ti = tid / N, tm = tid - ti * N;
     if (ti < ng) tagv = ld_relaxed_sys(tag_ptr(tm, t0 + ti));
+    // speculative entry u of this thread: (tile i, rank m, entry j) of flat
+    // index tid + u * kTileThreads, j fastest
+    auto spec_at = [&](int u, int& i, int& m, int& j) {
+        const int fl = tid + u * kTileThreads;
+        i = fl / (N * SP);
+        m = (fl / SP) % N;
+        j = fl % SP;
+    };
     unsigned spec[kSpecPerThread];
-    int sm_[kSpecPerThread], si_[kSpecPerThread], sj_[kSpecPerThread];
 #pragma unroll
     for (int u = 0; u < kSpecPerThread; ++u) {
-        const int fl = tid + u * kTileThreads;
-        si_[u] = fl / (N * SP);
-        sm_[u] = (fl / SP) % N;
-        sj_[u] = fl % SP;
+        int i, m, j;
+        spec_at(u, i, m, j);
         spec[u] = 0u;
-        if (si_[u] < ng) spec[u] = ld_relaxed_sys(entry_ptr(sm_[u], t0 + si_[u], sj_[u]));
+        if (i < ng) spec[u] = ld_relaxed_sys(entry_ptr(m, t0 + i, j));
     }
     int4* c4 = reinterpret_cast<int4*>(s_cnt);
     for (int q = tid; q < kDecGroup * kTile / 16; q += kTileThreads) c4[q] = make_int4(0, 0, 0, 0);
@@ -253,42 +246,100 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
         return;
     }
 
-    // ordered per-rank passes
+    // Entries beyond the speculative blocks ("overflow", dense tiles):
+    // exclusive prefix of their counts over the (tile, rank) pairs
+    __shared__ int s_ovo[kDecGroup * kFusedMaxRanks + 1];
+    if (tid < 32) {
+        int v[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int pr = 2 * tid + h;
+            v[h] = pr < ng * N ? max(0, s_k[(pr / N) * kFusedMaxRanks + pr % N] - SP) : 0;
+        }
+        int incl = v[0] + v[1];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        s_ovo[2 * tid] = incl - v[0] - v[1];
+        s_ovo[2 * tid + 1] = incl - v[1];
+        if (tid == 31) s_ovo[2 * 32] = incl;
+    }
+    __syncthreads();
+    const int OV = s_ovo[kDecGroup * kFusedMaxRanks];
     const unsigned stamp = entry_stamp(p.epoch);
+    const unsigned long long t_start = now_ns();
     bool ok = true;
-    for (int m = 0; m < N; ++m) {
+    // re-poll the stale entries of a batch together until all carry this
+    // step's stamp (the tag can land before the entries of its record)
+    auto settle = [&](unsigned* e, const unsigned** a, unsigned pend) {
+        while (pend && ok) {
+            __nanosleep(64);
+#pragma unroll
+            for (int u = 0; u < kSpecPerThread; ++u)
+                if ((pend >> u) & 1u) e[u] = ld_relaxed_sys(a[u]);
+#pragma unroll
+            for (int u = 0; u < kSpecPerThread; ++u)
+                if (((pend >> u) & 1u) && (e[u] >> kStampShift) == stamp) pend &= ~(1u << u);
+            if (pend && now_ns() - t_start > kTimeoutNs) ok = false;
+        }
+    };
+    {
+        const unsigned* a[kSpecPerThread];
+        unsigned pend = 0u;
 #pragma unroll
         for (int u = 0; u < kSpecPerThread; ++u) {
-            if (!ok || sm_[u] != m || si_[u] >= ng || sj_[u] >= s_k[si_[u] * kFusedMaxRanks + m]) continue;
-            unsigned e = spec[u];
-            if ((e >> kStampShift) != stamp && !await_entry(entry_ptr(m, t0 + si_[u], sj_[u]), stamp, e)) {
-                ok = false;
-                continue;
-            }
-            count_entry(s_cnt + si_[u] * kTile, e);
+            int i, m, j;
+            spec_at(u, i, m, j);
+            a[u] = entry_ptr(m, t0 + i, j);
+            if (i < ng && j < s_k[i * kFusedMaxRanks + m] && (spec[u] >> kStampShift) != stamp) pend |= 1u << u;
         }
-        // entries beyond the speculative block (dense tiles)
-        for (int i = 0; i < ng && ok; ++i) {
-            const int k = s_k[i * kFusedMaxRanks + m];
-            for (int j0 = SP + tid; j0 < k && ok; j0 += kWordBatch * kTileThreads) {
-                unsigned e[kWordBatch];
+        settle(spec, a, pend);
+    }
+    constexpr int kOvChunk = kSpecPerThread * kTileThreads;
+    for (int c0 = 0;; c0 += kOvChunk) {
+        unsigned ov[kSpecPerThread];
+        int opr[kSpecPerThread];
+        const unsigned* a[kSpecPerThread];
+        unsigned pend = 0u;
 #pragma unroll
-                for (int u = 0; u < kWordBatch; ++u)
-                    if (j0 + u * kTileThreads < k) e[u] = ld_relaxed_sys(entry_ptr(m, t0 + i, j0 + u * kTileThreads));
+        for (int u = 0; u < kSpecPerThread; ++u) {
+            const int fo = c0 + tid + u * kTileThreads;
+            opr[u] = -1;
+            a[u] = nullptr;
+            if (fo < OV) {
+                int lo = 0, hi = kDecGroup * kFusedMaxRanks;  // s_ovo[lo] <= fo < s_ovo[hi]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_ovo[mid] <= fo) lo = mid; else hi = mid;
+                }
+                opr[u] = lo;
+                a[u] = entry_ptr(lo % N, t0 + lo / N, SP + fo - s_ovo[lo]);
+                ov[u] = ld_relaxed_sys(a[u]);
+            }
+        }
 #pragma unroll
-                for (int u = 0; u < kWordBatch; ++u) {
-                    const int j = j0 + u * kTileThreads;
-                    if (j >= k || !ok) continue;
-                    if ((e[u] >> kStampShift) != stamp && !await_entry(entry_ptr(m, t0 + i, j), stamp, e[u])) {
-                        ok = false;
-                        continue;
-                    }
-                    count_entry(s_cnt + i * kTile, e[u]);
+        for (int u = 0; u < kSpecPerThread; ++u)
+            if (opr[u] >= 0 && (ov[u] >> kStampShift) != stamp) pend |= 1u << u;
+        settle(ov, a, pend);
+        if (!ok) *s_abort = 1;
+        // ordered per-rank passes over the batch (plus, first, the speculative entries)
+        for (int m = 0; m < N; ++m) {
+            if (c0 == 0) {
+#pragma unroll
+                for (int u = 0; u < kSpecPerThread; ++u) {
+                    int i, mm, j;
+                    spec_at(u, i, mm, j);
+                    if (ok && mm == m && i < ng && j < s_k[i * kFusedMaxRanks + m]) count_entry(s_cnt + i * kTile, spec[u]);
                 }
             }
+#pragma unroll
+            for (int u = 0; u < kSpecPerThread; ++u)
+                if (ok && opr[u] >= 0 && opr[u] % N == m) count_entry(s_cnt + (opr[u] / N) * kTile, ov[u]);
+            __syncthreads();  // the next rank's pass may touch the same counts
         }
-        if (!ok) *s_abort = 1;
-        __syncthreads();  // the next rank's pass may touch the same counts
+        if (c0 + kOvChunk >= OV) break;
     }
     stamp_ph(2);
     if (*s_abort) {

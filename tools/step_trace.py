@@ -34,6 +34,11 @@ def report(rank, tr):
     q = [int(ncta * i / 10) for i in range(10)] + [ncta - 1]
     print("  start at blockIdx deciles:", [round(float(st[i]), 1) for i in q], flush=True)
     print("  end   at blockIdx deciles:", [round(float(en[i]), 1) for i in q], flush=True)
+    print(f"  kernel first start (globaltimer) {int(ph[:, 0].min())}; last encode end {en[e].max():.1f} us", flush=True)
+    tail = np.nonzero(dec)[0][-int(os.environ.get("TRACE_TAIL", "12")):]
+    for i in tail:
+        print(f"    cta {i}: start {st[i]:.1f} tags {(ph[i, 1] - base) / 1e3:.1f} counts {(ph[i, 2] - base) / 1e3:.1f} "
+              f"end {en[i]:.1f}", flush=True)
 
 
 def main():
