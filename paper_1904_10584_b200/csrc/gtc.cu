@@ -653,6 +653,8 @@ static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual,
     p.k_acc = &c->ctrl->k_acc[c->epoch & 1u];
     p.k_next = &c->ctrl->k_acc[(c->epoch + 1u) & 1u];
     p.epoch = c->epoch;
+    p.buf = c->mom_buf;
+    p.mu = c->mom_mu;
     p.publish_sys = 1;
     p.num_tiles = c->num_tiles;
     p.tile_begin = 0;
@@ -710,7 +712,7 @@ gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* targe
     }
     if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1) {
         const int K = pipeline_chunks(c);
-        if (K == 1 && fused_step_enabled() && c->world <= kFusedMaxRanks && mode != GTC_ACCUM_MOMENTUM) {
+        if (K == 1 && fused_step_enabled() && c->world <= kFusedMaxRanks) {
             gtc_status s = check_encode_args(c, grad, residual);
             if (s == GTC_OK) s = check_apply_args(c, target, mode);
             if (s != GTC_OK) return s;

@@ -22,7 +22,8 @@
 //     within one rank's tile: no two threads of a pass touch one count, no
 //     atomics, deterministic).  Then u = fl(c * tau), WEIGHTS
 //     t = fmaf(alpha, u, t) / UPDATE t = fl(t + u) on the touched elements
-//     (R8), 128-bit read-modify-write of the float4s holding a non-zero count.
+//     (R8), 128-bit read-modify-write of the float4s holding a non-zero count;
+//     GTC_ACCUM_MOMENTUM: the dense SGD-momentum update (M1) of the tiles.
 // Why this shape: a CTA slot is held for its whole lifetime, and the encode is
 // bound by the HBM bytes its resident CTAs keep in flight.  Any NVLink round
 // trip a CTA waits for (~3-9 us while the peer's HBM is saturated by its own
@@ -347,6 +348,48 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
         return;
     }
 
+    if constexpr (MODE == GTC_ACCUM_MOMENTUM) {
+        // SGD-momentum (M1) over EVERY element of the tiles (an untouched
+        // weight still moves by its decaying momentum): u = fl(c * tau),
+        // buf = fl(fl(mu * buf) + u), w = fmaf(alpha, buf, w); float4 v of a
+        // tile is element 4v, thread tid takes v = tid + 256 h (coalesced),
+        // the tile's 4 float4 of w and of buf in flight together
+        for (int i = 0; i < ng; ++i) {
+            const long long tb = (t0 + i) * kTile;
+            float4 wv[kTileVec], bv[kTileVec];
+#pragma unroll
+            for (int h = 0; h < kTileVec; ++h) {
+                const long long e0 = tb + 4ll * (tid + h * kTileThreads);
+                if (e0 + 4 <= p.n) {
+                    wv[h] = ld_v4(reinterpret_cast<const float4*>(f.target + e0));
+                    bv[h] = ld_v4(reinterpret_cast<const float4*>(p.buf + e0));
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < kTileVec; ++h) {
+                const int v = tid + h * kTileThreads;
+                const long long e0 = tb + 4ll * v;
+                const int packed = reinterpret_cast<const int*>(s_cnt + i * kTile)[v];
+                auto mom = [&](float& w, float& bf, int e) {
+                    const float u = __fmul_rn((float)(int)(signed char)((unsigned)packed >> (8 * e)), p.tau);
+                    bf = __fadd_rn(__fmul_rn(p.mu, bf), u);
+                    w = __fmaf_rn(f.alpha, bf, w);
+                };
+                if (e0 + 4 <= p.n) {
+                    mom(wv[h].x, bv[h].x, 0);
+                    mom(wv[h].y, bv[h].y, 1);
+                    mom(wv[h].z, bv[h].z, 2);
+                    mom(wv[h].w, bv[h].w, 3);
+                    st_stream(reinterpret_cast<float4*>(f.target + e0), wv[h]);
+                    st_stream(reinterpret_cast<float4*>(p.buf + e0), bv[h]);
+                } else {
+                    for (int e = 0; e < 4 && e0 + e < p.n; ++e) mom(f.target[e0 + e], p.buf[e0 + e], e);
+                }
+            }
+        }
+        return;
+    }
+
     // apply: thread tid owns elements [16 tid, 16 tid + 16) of each tile, as
     // four float4 (bit i * 4 + h of `todo`: float4 h of tile i is touched)
     unsigned todo = 0u;
@@ -465,6 +508,7 @@ cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
 
 template <int CMP, bool HAS_G>
 cudaError_t launch_g(FusedStepParams& f, int mode, cudaStream_t s) {
+    if (mode == GTC_ACCUM_MOMENTUM) return launch_t<CMP, HAS_G, GTC_ACCUM_MOMENTUM>(f, s);
     return mode == GTC_ACCUM_UPDATE ? launch_t<CMP, HAS_G, GTC_ACCUM_UPDATE>(f, s)
                                     : launch_t<CMP, HAS_G, GTC_ACCUM_WEIGHTS>(f, s);
 }

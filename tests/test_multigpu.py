@@ -85,7 +85,8 @@ def test_pipelined_step_parity():
 
 
 @pytest.mark.parametrize("world,lag,accum", [(2, "1", "weights"), (2, "7", "update"), (3, "64", "weights"),
-                                             (4, "5", "weights"), (4, "0", "update")])
+                                             (4, "5", "weights"), (4, "0", "update"), (2, "0", "momentum"),
+                                             (4, "9", "momentum")])
 def test_fused_step_parity(world, lag, accum):
     """The fused one-kernel p2p step (step_p2p.cu) with short decode lags, so
     CTAs wait on peers' tiles still being written (stamped entries), and with
