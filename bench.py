@@ -69,6 +69,9 @@ def parse():
                     help="apply: sparse fmaf into the weights (headline) or the dense SGD-momentum update")
     ap.add_argument("--mu", type=float, default=0.9, help="SGD momentum for --accum momentum")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-step", action="store_true",
+                    help="world > 1, p2p: gtc_step as encode + decode_apply kernels (GTC_STEP_SPLIT) "
+                         "instead of the one fused kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -260,7 +263,8 @@ def run_gtc(args):
     # the contiguous message is only built on demand (gtc_message / NCCL mode):
     # at 1e9 params cap it at 5 % of n to save 3 GB per rank
     cap = 0 if n < 100_000_000 or args.exchange == "nccl" else n // 20
-    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp, exchange=args.exchange, max_words_per_rank=cap)
+    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp, exchange=args.exchange, max_words_per_rank=cap,
+                  fused_step=not args.split_step)
     stream = torch.cuda.current_stream(dev)
     momentum = args.accum == "momentum"
     amode = gtc.GTC_ACCUM_MOMENTUM if momentum else gtc.GTC_ACCUM_WEIGHTS
@@ -478,6 +482,7 @@ def run_gtc(args):
                    "parallelism": f"dp{world}",
                    "apply": f"ACCUM_MOMENTUM (mu={args.mu})" if momentum else "ACCUM_WEIGHTS",
                    "exchange": ctx.exchange_mode(),
+                   "step": "one kernel" if one_kernel else "separate kernels",
                    "l2": f"inputs larger than L2: g rotates over {NB} buffer(s), "
                          f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": enc_gbs, "peak": peak,

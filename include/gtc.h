@@ -92,6 +92,12 @@ enum { GTC_EXCHANGE_P2P = 0,     /* default: peers' messages are read straight f
        GTC_EXCHANGE_NCCL = 16    /* ncclAllGather of counts, one host wait, then
                                     ncclAllGather of the words and tile offsets  */ };
 
+/* gtc_step at world > 1 with the p2p exchange (OR-ed into gtc_init's flags). */
+enum { GTC_STEP_FUSED = 0,       /* default: the whole step is ONE kernel
+                                    (gtc_step_p2p_kernel)     */
+       GTC_STEP_SPLIT = 32       /* encode + decode_apply as two kernels: faster
+                                    above ~5 % update density */ };
+
 /* What decode_apply updates (R8, M1). */
 enum { GTC_ACCUM_WEIGHTS = 0, /* target[i] = fmaf(alpha, fl(c[i]*tau), target[i]) */
        GTC_ACCUM_UPDATE = 1,  /* target[i] = fl(target[i] + fl(c[i]*tau))        */
@@ -117,7 +123,8 @@ gtc_status gtc_get_unique_id(void* out_128_bytes);
  *  nccl_unique_id : 128 bytes from gtc_get_unique_id on rank 0; NULL iff world == 1.
  *  cuda_device: device ordinal this rank runs on (made current for the call).
  *  flags      : GTC_CMP_GT or GTC_CMP_GE, OR-ed with GTC_EXCHANGE_P2P (default) or
- *               GTC_EXCHANGE_NCCL.
+ *               GTC_EXCHANGE_NCCL, OR-ed with GTC_STEP_FUSED (default) or
+ *               GTC_STEP_SPLIT.  Other bits: GTC_EINVAL.
  * On success *out is a new context (free with gtc_destroy). Blocks on NCCL
  * communicator creation when world > 1. */
 gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int world,
@@ -192,9 +199,14 @@ gtc_status gtc_decode_apply(gtc_ctx* ctx, float* target, float alpha, int mode,
 gtc_status gtc_bind_momentum(gtc_ctx* ctx, float* buf, float mu);
 
 /* One whole step: gtc_encode, gtc_exchange, gtc_decode_apply in one call
- * (same arguments and semantics; returns the first failing status, or
- * GTC_ENONFINITE from the exchange after completing the step).  Saves the
- * per-call overhead of three calls on launch-bound sizes. */
+ * (same arguments and results; returns the first failing status, or
+ * GTC_ENONFINITE from the exchange after completing the step).  It is ONE
+ * kernel launch at world 1 (the encode applies the rank's own quanta) and, by
+ * default, at world > 1 with the p2p exchange (PAPER.md:222 encode ->
+ * exchange -> aggregate -> apply fused); there device-side
+ * faults (GTC_EPEER, GTC_ENONFINITE) are sticky and reported by gtc_check.
+ * GTC_STEP_SPLIT, GTC_ACCUM_* all supported; GTC_EXCHANGE_NCCL runs the
+ * three calls. */
 gtc_status gtc_step(gtc_ctx* ctx, const float* grad, float* residual, float* target, float alpha,
                     int mode, cudaStream_t stream);
 

@@ -37,6 +37,8 @@ GTC_CMP_GT = 0
 GTC_CMP_GE = 1
 GTC_EXCHANGE_P2P = 0
 GTC_EXCHANGE_NCCL = 16
+GTC_STEP_FUSED = 0
+GTC_STEP_SPLIT = 32
 GTC_ACCUM_WEIGHTS = 0
 GTC_ACCUM_UPDATE = 1
 GTC_ACCUM_MOMENTUM = 2
@@ -290,7 +292,7 @@ class GTC:
 
     def __init__(self, n_params: int, tau: float, rank: int = 0, world: int = 1, device=None,
                  cmp: str = "gt", max_words_per_rank: int = 0, max_sim_msgs: int = 0, group=None,
-                 exchange: str = "p2p"):
+                 exchange: str = "p2p", fused_step: bool = True):
         import torch
 
         if not torch.cuda.is_available():
@@ -299,6 +301,7 @@ class GTC:
         self.n, self.tau, self.rank, self.world = int(n_params), float(tau), int(rank), int(world)
         self.cmp = {"gt": GTC_CMP_GT, "ge": GTC_CMP_GE}[cmp]
         flags = self.cmp | {"p2p": GTC_EXCHANGE_P2P, "nccl": GTC_EXCHANGE_NCCL}[exchange]
+        flags |= GTC_STEP_FUSED if fused_step else GTC_STEP_SPLIT
         self.max_words = max_words_per_rank if max_words_per_rank > 0 else self.n
         uid = None
         if world > 1:

@@ -104,6 +104,7 @@ struct gtc_ctx {
     int rank = 0, world = 1, device = 0;
     int cmp_mode = GTC_CMP_GT;
     bool p2p = false;
+    bool split_step = false;        // GTC_STEP_SPLIT: gtc_step as encode + decode_apply kernels
     int num_tiles = 0;
     ncclComm_t comm = nullptr;
 
@@ -270,7 +271,7 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     if (!(tau > 0.f) || std::isinf(tau)) return GTC_EINVAL;
     if (world < 1 || rank < 0 || rank >= world) return GTC_EINVAL;
     if (world > GTC_MAX_MSGS) return GTC_EUNSUPPORTED;
-    if (flags & ~(uint32_t)(GTC_CMP_GE | GTC_EXCHANGE_NCCL)) return GTC_EINVAL;
+    if (flags & ~(uint32_t)(GTC_CMP_GE | GTC_EXCHANGE_NCCL | GTC_STEP_SPLIT)) return GTC_EINVAL;
     if ((world > 1) != (nccl_unique_id != nullptr)) return GTC_EINVAL;
 
     gtc_ctx* c = new (std::nothrow) gtc_ctx();
@@ -282,6 +283,7 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     c->device = cuda_device;
     c->cmp_mode = (int)(flags & GTC_CMP_GE);
     c->p2p = world > 1 && !(flags & GTC_EXCHANGE_NCCL);
+    c->split_step = (flags & GTC_STEP_SPLIT) != 0;
     c->num_tiles = (int)((n_params + kTile - 1) / kTile);
     c->last_k.assign(world, 0);
 
@@ -712,7 +714,7 @@ gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* targe
     }
     if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1) {
         const int K = pipeline_chunks(c);
-        if (K == 1 && fused_step_enabled() && c->world <= kFusedMaxRanks) {
+        if (K == 1 && !c->split_step && fused_step_enabled() && c->world <= kFusedMaxRanks) {
             gtc_status s = check_encode_args(c, grad, residual);
             if (s == GTC_OK) s = check_apply_args(c, target, mode);
             if (s != GTC_OK) return s;

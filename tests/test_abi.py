@@ -54,6 +54,10 @@ def test_host_side_validation_without_gpu():
         gtc.gtc_init(10, 8.0, rank=1, world=1)
     with pytest.raises(gtc.GTCError):
         gtc.gtc_init(10, 8.0, world=2)  # world > 1 needs a unique id
+    with pytest.raises(gtc.GTCError) as e:
+        gtc.gtc_init(10, 8.0, flags=64)  # no such flag bit
+    assert e.value.status == gtc.GTC_EINVAL
+    assert gtc.GTC_STEP_SPLIT & (gtc.GTC_CMP_GE | gtc.GTC_EXCHANGE_NCCL) == 0
     assert gtc.gtc_strerror(gtc.GTC_ECORRUPT) == "corrupt message"
 
 
