@@ -4,7 +4,8 @@
 //
 // Messages come in two layouts (gtc_internal.cuh): SEGMENTED (the hot path:
 // words of tile t in slot t of a tile-major buffer, tag[t] = epoch<<32 |
-// count; in p2p mode the peers' buffers are read straight over NVLink) or
+// count; in p2p mode the peers' buffers are read straight over NVLink, and
+// their stamped entries are turned back into words, entry_word) or
 // CONTIGUOUS (NCCL all-gather, caller messages: words + per-tile offsets).
 //
 // gtc_decode_apply_kernel (any number of messages):

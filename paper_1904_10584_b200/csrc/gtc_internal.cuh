@@ -47,15 +47,20 @@ struct MsgHeader {
 };
 
 // ---------------------------------------------------------------- messages
-// The hot path's message is SEGMENTED: encode kernel 1 compacts the words of
-// tile t (ascending index) into slot t of a tile-major buffer,
+// The hot path's message is SEGMENTED: the encode compacts the words of tile
+// t (ascending index) into slot t of a tile-major buffer,
 //     words of tile t = seg[t * kTile .. t * kTile + count_t),
-// and tag[t] = (epoch << 32) | count_t.  In p2p mode the rank publishes the
-// whole message by raising Ctrl::ready[slot] = step after a system-scope
-// fence -- done by block 0 of its decode kernel (stream order puts every
-// encode store before it), or by a one-thread publish kernel per chunk in the
-// pipelined gtc_step -- and peers acquire that flag before reading over NVLink.  Decode reads exactly the words of the tiles it owns, from
-// every rank, without a global prefix scan.
+// and tag[t] = (epoch << 32) | count_t.  In p2p mode a slot holds STAMPED
+// tile-local entries instead (tile_encode.cuh: stamp(epoch) << 13 | local << 1
+// | neg), so a reader can tell this step's entries from older ones without a
+// writer-side fence.  The separate calls publish the whole message by raising
+// Ctrl::ready[slot] = step after a system-scope fence -- done by block 0 of the
+// decode kernel (stream order puts every encode store before it), or by a
+// one-thread publish kernel per chunk in the pipelined gtc_step -- and peers
+// acquire that flag before reading over NVLink; the fused step
+// (step_p2p.cu) instead pushes per-tile records and checks stamps.  Decode
+// reads exactly the words of the tiles it owns, from every rank, without a
+// global prefix scan.
 // The CONTIGUOUS message (words in one array + per-tile offsets + header) is
 // the wire format of the NCCL exchange and of gtc_message; gtc_compact_kernel
 // builds it from a segmented one on demand.
