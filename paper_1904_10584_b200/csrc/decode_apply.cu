@@ -556,16 +556,6 @@ __global__ void gtc_tile_bounds_kernel(const BoundsParams p) {
     if (bad) atomicOr(p.flags, kFlagCorrupt);
 }
 
-// Programmatic dependent launch of the decode kernels (GTC_PDL=0 disables).
-bool pdl_on() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("GTC_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-
 int sm_count() {
     static int sms = 0;
     if (sms == 0) {
@@ -620,7 +610,7 @@ cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute la[1];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    la[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    la[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = la;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
@@ -649,7 +639,7 @@ cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
             cfg.stream = s;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+            attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             return cudaLaunchKernelEx(&cfg, gtc_apply_single_seg_kernel<MODE>, p);

@@ -559,15 +559,6 @@ int encode_variant() {
 }
 bool use_persistent() { return encode_variant() == 1; }
 
-// Programmatic dependent launch of the encode kernel (GTC_PDL=0 disables).
-bool pdl_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("GTC_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
 
 template <int CMP, bool HAS_G>
 cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
@@ -601,6 +592,16 @@ cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
 }
 
 }  // namespace
+
+// Programmatic dependent launch of every hot-path kernel (GTC_PDL=0 disables).
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
 
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s) {
     if (p.num_tiles == 0) return cudaSuccess;

@@ -183,6 +183,7 @@ IpcResult ipc_map_peers(ncclComm_t comm, int rank, int world, unsigned char* loc
                         unsigned char* slots, std::vector<unsigned char*>& peers, std::vector<void*>& allocs);
 void ipc_unmap(std::vector<void*>& allocs);
 
+bool pdl_enabled();  // programmatic dependent launch (GTC_PDL=0 disables)
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
 cudaError_t launch_publish(Ctrl* ctrl, int slot, unsigned long long step, cudaStream_t s);

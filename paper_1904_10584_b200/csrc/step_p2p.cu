@@ -482,15 +482,6 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_step_p2p_kernel(const Fus
     stamp_ph(4);
 }
 
-bool pdl_wanted() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("GTC_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-
 template <int CMP, bool HAS_G, int MODE>
 cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
@@ -500,7 +491,7 @@ cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_wanted() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, gtc_step_p2p_kernel<CMP, HAS_G, MODE>, f);
