@@ -456,9 +456,12 @@ def run_gtc(args):
     dec_bytes = 4 * sum_k + 8 * world * ntiles + (16 * n if momentum else 8 * nnz_c)
     dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9 if world > 1 and dec_ms > 0 else None
     step_bytes = enc_bytes + (dec_bytes + 4 * (world - 1) * max(k_all) if world > 1 and not one_kernel else 0)
+    # DRAM traffic per launch from the committed ncu capture of the encode
+    # kernel; none for the world > 1 one-kernel step (ncu cannot replay it:
+    # its CTAs wait on the peers' pushes)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "encode_dram_bytes.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and not (world > 1 and one_kernel):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
