@@ -441,9 +441,10 @@ def run_gtc(args):
     elif one_kernel:
         # the fused p2p step kernel, local HBM: the encode (12 n + 4 k + 8 T),
         # this rank's words and tags read back by the decode (4 k + 8 T), the
-        # target read-modify-write of the touched elements (8 nnz); the peers'
+        # target read-modify-write of the touched elements (8 nnz; momentum:
+        # w and buf read and written, 16 n); the peers'
         # words and tags cross NVLink (nvlink_bytes_per_rank)
-        enc_bytes = 12 * n + 8 * k_rank + 16 * ntiles + 8 * nnz_c
+        enc_bytes = 12 * n + 8 * k_rank + 16 * ntiles + (16 * n if momentum else 8 * nnz_c)
         nvl_bytes = 4 * (sum(k_all) - k_rank) + 8 * (world - 1) * ntiles
         kernel_name = "gtc_step_p2p_kernel (fused encode + exchange + decode + apply)"
     else:
@@ -461,7 +462,7 @@ def run_gtc(args):
     # its CTAs wait on the peers' pushes)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "encode_dram_bytes.json")
-    if os.path.exists(tpath) and not (world > 1 and one_kernel):
+    if os.path.exists(tpath) and not (world > 1 and one_kernel) and not momentum:
         try:
             with open(tpath) as f:
                 tj = json.load(f)
