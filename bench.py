@@ -445,7 +445,7 @@ def run_gtc(args):
         # w and buf read and written, 16 n); the peers'
         # words and tags cross NVLink (nvlink_bytes_per_rank)
         enc_bytes = 12 * n + 8 * k_rank + 16 * ntiles + (16 * n if momentum else 8 * nnz_c)
-        nvl_bytes = 4 * (sum(k_all) - k_rank) + 8 * (world - 1) * ntiles
+        nvl_bytes = 4 * (sum(k_all) - k_rank) + 16 * (world - 1) * ntiles  # records: 16-byte header + entries
         kernel_name = "gtc_step_p2p_kernel (fused encode + exchange + decode + apply)"
     else:
         enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles
