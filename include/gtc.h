@@ -77,8 +77,15 @@ typedef enum {
     GTC_ESTATE = 8,      /* call out of order / workspace not bound              */
     GTC_ECAPACITY = 9,   /* a message exceeded max_words_per_rank                 */
     GTC_EUNSUPPORTED = 10,/* e.g. world > GTC_MAX_MSGS, p2p mapping impossible   */
-    GTC_EPEER = 11       /* p2p: a peer did not publish its message within 30 s
-                            (nothing was applied)                                 */
+    GTC_EPEER = 11       /* a peer did not publish its message within the timeout
+                            (GTC_PEER_TIMEOUT_MS, default 30 s).  p2p: raised on
+                            EVERY rank (the rank that timed out sets it in each
+                            rank's flags over NVLink); the step is INCOMPLETE --
+                            some tiles may have been applied on some ranks, so
+                            weights/residuals are no longer consistent replicas:
+                            restore them from a checkpoint.  NCCL mode: this
+                            rank's communicator was aborted (ncclCommAbort) and
+                            the context accepts no further steps.               */
 } gtc_status;
 
 /* Threshold comparison (R1). */
@@ -97,6 +104,18 @@ enum { GTC_STEP_FUSED = 0,       /* default: the whole step is ONE kernel
                                     (gtc_step_p2p_kernel)     */
        GTC_STEP_SPLIT = 32       /* encode + decode_apply as two kernels: faster
                                     above ~5 % update density */ };
+
+/* gtc_init flag: one rank of a LOOPBACK group -- all `world` ranks are
+ * contexts of ONE process (tests and single-process drivers; no NCCL
+ * communicator, no CUDA IPC, nccl_unique_id must be NULL, p2p exchange,
+ * world <= 8).  After every rank's gtc_bind_workspace, gtc_connect_loopback
+ * links them.  A rank's gtc_exchange then launches a one-thread publish
+ * kernel; the group steps either with the separate calls (every rank's
+ * gtc_encode, then every rank's gtc_exchange, then every rank's
+ * gtc_decode_apply, in that order, so no kernel waits on one not yet queued)
+ * or with gtc_step_group (the fused step of all ranks as ONE launch).
+ * gtc_step on a loopback context returns GTC_EUNSUPPORTED. */
+enum { GTC_LOOPBACK = 64 };
 
 /* What decode_apply updates (R8, M1). */
 enum { GTC_ACCUM_WEIGHTS = 0, /* target[i] = fmaf(alpha, fl(c[i]*tau), target[i]) */
@@ -124,7 +143,10 @@ gtc_status gtc_get_unique_id(void* out_128_bytes);
  *  cuda_device: device ordinal this rank runs on (made current for the call).
  *  flags      : GTC_CMP_GT or GTC_CMP_GE, OR-ed with GTC_EXCHANGE_P2P (default) or
  *               GTC_EXCHANGE_NCCL, OR-ed with GTC_STEP_FUSED (default) or
- *               GTC_STEP_SPLIT.  Other bits: GTC_EINVAL.
+ *               GTC_STEP_SPLIT, optionally OR-ed with GTC_LOOPBACK (then
+ *               nccl_unique_id is NULL).  Other bits: GTC_EINVAL.
+ * The environment variable GTC_PEER_TIMEOUT_MS (read here) sets how long a
+ * p2p kernel, or the NCCL-mode host wait, waits for a peer (default 30000).
  * On success *out is a new context (free with gtc_destroy). Blocks on NCCL
  * communicator creation when world > 1. */
 gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int world,
@@ -164,8 +186,9 @@ gtc_status gtc_bind_workspace(gtc_ctx* ctx, void* dev_ptr, size_t bytes,
 gtc_status gtc_encode(gtc_ctx* ctx, const float* grad, float* residual, cudaStream_t stream);
 
 /* Make every rank's message available to every other rank (world > 1).
- *  p2p : one single-warp kernel publishes "step e ready" into every peer's
- *        ready flags over NVLink (release, system scope); no host wait.
+ *  p2p : no device work (decode_apply raises this rank's ready flag, release
+ *        at system scope, and reads the peers' tiles in place); loopback
+ *        group: a one-thread kernel raises the ready flag.  No host wait.
  *        Errors of any rank are reported by gtc_check after decode_apply.
  *  nccl: ncclAllGather of (k, flags), ONE host wait for the counts, then
  *        ncclAllGather of the words padded to the largest k and of the
@@ -175,10 +198,12 @@ gtc_status gtc_encode(gtc_ctx* ctx, const float* grad, float* residual, cudaStre
  * world == 1: no device work. */
 gtc_status gtc_exchange(gtc_ctx* ctx, cudaStream_t stream);
 
-/* Steps 5-6 of P:222 on `stream` (p2p: the kernel first waits, on the device,
- * for every peer's ready flag of this step, then reads the peers' messages
- * over NVLink; if any rank overflowed its capacity or a peer timed out,
- * nothing is applied and gtc_check reports it): signed integer counts of all ranks' quanta
+/* Steps 5-6 of P:222 on `stream` (p2p: the kernel first raises this rank's
+ * ready flag, waits on the device for every peer's ready flag of this step,
+ * then reads the peers' messages over NVLink; if a peer misses the timeout,
+ * the CTAs that timed out apply nothing and every rank's gtc_check reports
+ * GTC_EPEER; if this rank's message overflowed its capacity nothing is
+ * applied): signed integer counts of all ranks' quanta
  * (deterministic, atomic-free, rank order irrelevant) and the apply of
  * count * tau to target (float[n] device, in/out) for every element with a
  * non-zero count (mode GTC_ACCUM_WEIGHTS with alpha, or GTC_ACCUM_UPDATE), or
@@ -236,10 +261,36 @@ gtc_status gtc_message(gtc_ctx* ctx, int rank, const uint32_t** dev_words, int64
  * debugging; waits for the device).  max_words is the room at host_words. */
 gtc_status gtc_read_message(gtc_ctx* ctx, int rank, uint32_t* host_words, int64_t max_words, int64_t* k);
 
-/* Wait for `stream`, then report and clear the sticky device flags:
- * GTC_EPEER, GTC_ECAPACITY, GTC_ECORRUPT, GTC_ENONFINITE or GTC_OK (p2p: the
- * flags of every rank of the last decode_apply are folded in). */
+/* Wait for `stream`, then report and clear this rank's sticky device flags:
+ * GTC_EPEER, GTC_ECAPACITY, GTC_ECORRUPT, GTC_ENONFINITE or GTC_OK.  A peer
+ * timeout anywhere in a p2p step is raised in EVERY rank's flags, so every
+ * rank's gtc_check reports GTC_EPEER (see GTC_EPEER for what it means). */
 gtc_status gtc_check(gtc_ctx* ctx, cudaStream_t stream);
+
+/* Loopback group (GTC_LOOPBACK): ctxs[r] is rank r of `world`, every one
+ * created with GTC_LOOPBACK and the same n, tau and flags, and bound with the
+ * same sizes.  Gives every rank a view of every rank's workspace (same
+ * process: plain device pointers; ranks on other devices: peer access is
+ * enabled).  GTC_EINVAL / GTC_ESTATE on a mismatched or unbound rank. */
+gtc_status gtc_connect_loopback(gtc_ctx* const* ctxs, int world);
+
+/* Loopback group, every rank on ONE device: the fused one-kernel step
+ * (PAPER.md:222 encode -> exchange -> aggregate -> apply; the kernel of
+ * gtc_step at world > 1) of all `world` ranks as ONE launch on `stream`:
+ * CTA j of rank r is block j * world + r, so every CTA a decode CTA waits on
+ * has a lower block index, exactly as in the per-rank kernel.
+ *  grads[r] / residuals[r] / targets[r]: rank r's arguments of gtc_step
+ *  (grads == NULL, or grads[r] == NULL on every rank: residuals hold r + g).
+ *  debug_flags: bit r set = rank r's CTAs exit at once (a rank that never
+ *  shows up: the others raise GTC_EPEER after the timeout); 0 in normal use.
+ * Waits for `stream` first (the parameters are staged in pinned memory). */
+gtc_status gtc_step_group(gtc_ctx* const* ctxs, int world, const float* const* grads, float* const* residuals,
+                          float* const* targets, float alpha, int mode, uint32_t debug_flags, cudaStream_t stream);
+
+/* Collective (every rank calls it; world > 1, p2p, not loopback): wait for
+ * the device, then an NCCL barrier, so no peer is still reading this rank's
+ * workspace.  Call it before gtc_destroy and before freeing the workspace. */
+gtc_status gtc_quiesce(gtc_ctx* ctx);
 
 /* GTC_EXCHANGE_P2P or GTC_EXCHANGE_NCCL (world > 1), 0 for world == 1. */
 int gtc_exchange_mode(const gtc_ctx* ctx);
@@ -264,7 +315,9 @@ gtc_status gtc_debug_step_trace(uint64_t* host, int max_entries);
 const char* gtc_strerror(gtc_status status);
 const char* gtc_last_error_detail(const gtc_ctx* ctx);
 
-/* Destroy the NCCL communicator and host state; never frees caller memory. */
+/* Destroy the NCCL communicator, the peer mappings and host state; never
+ * frees caller memory.  Local: no collective (run gtc_quiesce on every rank
+ * first when peers may still read this workspace). */
 void gtc_destroy(gtc_ctx* ctx);
 
 #ifdef __cplusplus

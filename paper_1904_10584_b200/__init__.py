@@ -39,6 +39,7 @@ GTC_EXCHANGE_P2P = 0
 GTC_EXCHANGE_NCCL = 16
 GTC_STEP_FUSED = 0
 GTC_STEP_SPLIT = 32
+GTC_LOOPBACK = 64
 GTC_ACCUM_WEIGHTS = 0
 GTC_ACCUM_UPDATE = 1
 GTC_ACCUM_MOMENTUM = 2
@@ -64,6 +65,9 @@ _SIGS = {
     "gtc_message": (_i32, [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]),
     "gtc_read_message": (_i32, [_vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]),
     "gtc_check": (_i32, [_vp, _vp]),
+    "gtc_connect_loopback": (_i32, [_vp, _i32]),
+    "gtc_step_group": (_i32, [_vp, _i32, _vp, _vp, _vp, _f32, _i32, _u32, _vp]),
+    "gtc_quiesce": (_i32, [_vp]),
     "gtc_exchange_mode": (_i32, [_vp]),
     "gtc_kernel_launches": (_i64, [_vp]),
     "gtc_debug_decode_trace": (_i32, [_vp, _i32]),
@@ -216,6 +220,26 @@ def gtc_check(ctx, stream: int) -> int:
     return load_library().gtc_check(ctx, stream)
 
 
+def gtc_connect_loopback(ctxs):
+    arr = (_vp * len(ctxs))(*[c.value if isinstance(c, _vp) else c for c in ctxs])
+    _chk(load_library().gtc_connect_loopback(arr, len(ctxs)), "gtc_connect_loopback", ctxs[0])
+
+
+def gtc_step_group(ctxs, grad_ptrs, residual_ptrs, target_ptrs, alpha: float, mode: int, debug_flags: int,
+                   stream: int) -> int:
+    w = len(ctxs)
+    C = (_vp * w)(*[c.value if isinstance(c, _vp) else c for c in ctxs])
+    G = (_vp * w)(*grad_ptrs) if grad_ptrs is not None else None
+    R = (_vp * w)(*residual_ptrs)
+    T = (_vp * w)(*target_ptrs)
+    return _chk(load_library().gtc_step_group(C, w, G, R, T, alpha, mode, debug_flags, stream), "gtc_step_group",
+                ctxs[0], ok=(GTC_OK, GTC_ENONFINITE))
+
+
+def gtc_quiesce(ctx):
+    _chk(load_library().gtc_quiesce(ctx), "gtc_quiesce", ctx)
+
+
 def gtc_kernel_launches(ctx) -> int:
     return load_library().gtc_kernel_launches(ctx)
 
@@ -287,12 +311,13 @@ class GTC:
 
     ``world > 1`` needs an initialised torch.distributed group (any backend)
     to broadcast the 128-byte NCCL id from rank 0; the exchange itself runs on
-    libgtc's own NCCL communicator.
+    libgtc's own NCCL communicator.  ``loopback=True``: one rank of an
+    in-process group (no NCCL, no torch.distributed; see ``LoopbackGroup``).
     """
 
     def __init__(self, n_params: int, tau: float, rank: int = 0, world: int = 1, device=None,
                  cmp: str = "gt", max_words_per_rank: int = 0, max_sim_msgs: int = 0, group=None,
-                 exchange: str = "p2p", fused_step: bool = True):
+                 exchange: str = "p2p", fused_step: bool = True, loopback: bool = False):
         import torch
 
         if not torch.cuda.is_available():
@@ -302,9 +327,12 @@ class GTC:
         self.cmp = {"gt": GTC_CMP_GT, "ge": GTC_CMP_GE}[cmp]
         flags = self.cmp | {"p2p": GTC_EXCHANGE_P2P, "nccl": GTC_EXCHANGE_NCCL}[exchange]
         flags |= GTC_STEP_FUSED if fused_step else GTC_STEP_SPLIT
+        self.loopback = bool(loopback)
+        if self.loopback:
+            flags |= GTC_LOOPBACK
         self.max_words = max_words_per_rank if max_words_per_rank > 0 else self.n
         uid = None
-        if world > 1:
+        if world > 1 and not self.loopback:
             uid = broadcast_unique_id(rank, group)
         with torch.cuda.device(self.device):
             self.ctx = gtc_init(self.n, self.tau, rank, world, uid, self.device.index, flags)
@@ -430,15 +458,75 @@ class GTC:
         return gtc_kernel_launches(self.ctx)
 
     def close(self):
+        """Collective at world > 1 (every rank calls it): quiesce (device sync +
+        NCCL barrier, so no peer still reads this workspace), then destroy."""
         if getattr(self, "ctx", None) is not None:
-            gtc_destroy(self.ctx)
-            self.ctx = None
+            try:
+                if self.world > 1 and not self.loopback:
+                    gtc_quiesce(self.ctx)
+            finally:
+                gtc_destroy(self.ctx)
+                self.ctx = None
 
     def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
+        # never a collective here: ranks collect garbage at different times
+        if getattr(self, "ctx", None) is not None:
+            try:
+                gtc_destroy(self.ctx)
+            except Exception:
+                pass
+            self.ctx = None
+
+
+class LoopbackGroup:
+    """``world`` ranks of one data-parallel group inside ONE process
+    (GTC_LOOPBACK contexts linked by gtc_connect_loopback): the real p2p
+    kernels with every rank's workspace a plain device pointer.  For tests and
+    single-process drivers; all ranks on ``device``.
+
+    ``step`` runs the fused one-kernel step of every rank as ONE launch
+    (gtc_step_group); ``split_step`` runs every rank's encode, then every
+    rank's exchange, then every rank's decode_apply (the separate calls)."""
+
+    def __init__(self, n_params: int, tau: float, world: int, device=None, cmp: str = "gt",
+                 max_words_per_rank: int = 0):
+        import torch
+
+        self.world = int(world)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.ranks = [GTC(n_params, tau, r, world, self.device, cmp=cmp, max_words_per_rank=max_words_per_rank,
+                          loopback=True) for r in range(world)]
+        gtc_connect_loopback([g.ctx for g in self.ranks])
+
+    def step(self, grads, residuals, targets, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS,
+             debug_flags: int = 0, stream=None) -> int:
+        gp = None if grads is None else [_ptr(g, "grad") for g in grads]
+        return gtc_step_group([g.ctx for g in self.ranks], gp, [_ptr(r, "residual") for r in residuals],
+                              [_ptr(t, "target") for t in targets], alpha, mode, debug_flags,
+                              _stream(stream, self.device))
+
+    def split_step(self, grads, residuals, targets, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS,
+                   counts_out=None, stream=None):
+        """counts_out: None or a list of int8[n] device tensors, one per rank."""
+        sts = []
+        for r, g in enumerate(self.ranks):
+            g.encode(None if grads is None else grads[r], residuals[r], stream)
+        for g in self.ranks:
+            sts.append(g.exchange(stream))
+        for r, g in enumerate(self.ranks):
+            g.decode_apply(targets[r], alpha, mode, None if counts_out is None else counts_out[r], stream)
+        return sts
+
+    def bind_momentum(self, bufs, mu: float):
+        for g, b in zip(self.ranks, bufs):
+            g.bind_momentum(b, mu)
+
+    def check(self, stream=None):
+        return [g.check(stream) for g in self.ranks]
+
+    def close(self):
+        for g in self.ranks:
+            g.close()
 
 
 # ----------------------------------------------------------------- BMUF (include/bmuf.h)

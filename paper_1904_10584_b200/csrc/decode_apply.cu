@@ -49,7 +49,6 @@ constexpr int kPreMsgs = 8;             // messages whose first words are preloa
 constexpr int kBatch = 8;               // words loaded per thread before their count updates
 constexpr int kMaxTouched = 2048;       // non-zero counts applied through the list (else dense fallback)
 constexpr int kChunksPerThread = kDecMaxTilesPerCta * (kTile / 16) / kDecThreads;
-constexpr unsigned long long kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000;
 
 // Opt-in phase trace of the counting decode (GTC_DECODE_TRACE=1): thread 0 of
 // each of the first kTraceCtas CTAs stamps %globaltimer at kTracePhases
@@ -71,15 +70,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 // p2p: wait (acquire, system scope) until rank m has published this step's
-// message (its last encode CTA raised ready = step).  A peer can be at most
-// one step ahead (its next decode waits for this rank), hence >=.  False on
-// timeout.
+// message (ready = step).  A peer can be at most one step ahead (its next
+// decode waits for this rank), hence >=.  False on timeout.
 __device__ __forceinline__ bool wait_ready(const DecodeParams& p, int m) {
     unsigned long long v = ld_acquire_sys(p.ready[m]);
     if (v >= p.step) return true;
     const unsigned long long t0 = globaltimer_ns();
     while (v < p.step) {
-        if (globaltimer_ns() - t0 > kPeerTimeoutNs) return false;
+        if (globaltimer_ns() - t0 > p.timeout_ns) return false;
         __nanosleep(64);
         v = ld_acquire_sys(p.ready[m]);
     }
@@ -217,8 +215,8 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
     // message density varies by parameter segment, and striding spreads the
     // dense segments' words evenly over the CTAs
     const int G = (int)gridDim.x;
-    const int t0 = p.tile_begin + (int)blockIdx.x;
-    const int nt = min(p.tiles_per_cta, (p.tile_end - t0 + G - 1) / G);
+    const int t0 = (int)blockIdx.x;
+    const int nt = min(p.tiles_per_cta, (p.num_tiles - t0 + G - 1) / G);
     const float inv_g = 1.0f / (float)G;
     auto tile_of = [&](int i) -> long long { return (long long)t0 + (long long)i * G; };
     // local count index (slot * kTile + offset) <-> parameter index
@@ -243,7 +241,9 @@ __global__ void __launch_bounds__(kDecThreads) gtc_decode_apply_kernel(const Dec
             __syncthreads();
             stamp(1);
             if (s_abort) {
-                if (tid == 0) atomicOr(p.flags, kFlagPeer);
+                // every rank learns of the timeout (gtc_check on any rank
+                // reports GTC_EPEER); this CTA applies nothing
+                for (int m = tid; m < p.nmsg; m += kDecThreads) atomicOr_system(p.peer_flags[m], kFlagPeer);
                 return;
             }
         }
@@ -579,7 +579,7 @@ cudaError_t launch_general(const DecodeParams& p_in, cudaStream_t s) {
     if (attr != cudaSuccess) return attr;
     DecodeParams p = p_in;
     const int sms = sm_count();
-    const int range = p.tile_end - p.tile_begin;
+    const int range = p.num_tiles;
     if (range <= 0) return cudaSuccess;
     // smallest tiles_per_cta whose grid fits in one wave of resident CTAs
     // (GTC_DECODE_TPC overrides, for measurement)
@@ -629,8 +629,7 @@ bool force_general() {
 
 template <int MODE>
 cudaError_t launch_mode(const DecodeParams& p, cudaStream_t s) {
-    if (MODE != GTC_ACCUM_MOMENTUM && p.nmsg == 1 && p.counts_out == nullptr && !p.wait && !force_general() &&
-        p.tile_begin == 0 && p.tile_end == p.num_tiles) {
+    if (MODE != GTC_ACCUM_MOMENTUM && p.nmsg == 1 && p.counts_out == nullptr && !p.wait && !force_general()) {
         if (p.segmented) {
             const int grid = (int)std::min<long long>((p.num_tiles + 7) / 8, (long long)sm_count() * 8);
             cudaLaunchConfig_t cfg = {};

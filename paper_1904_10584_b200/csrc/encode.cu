@@ -24,14 +24,17 @@
 //   - world 1 (gtc_step): the rank's own quanta are the aggregate (c = +-1),
 //     so the kernel also applies them to the target (loads issued right after
 //     the threshold test to hide their latency);
-//   - p2p: gtc_publish_kernel follows (system fence + the rank's ready flag).
-// gtc_encode_tiles_kernel (GTC_ENCODE_VARIANT=persistent, kept for
-//   measurement): persistent CTAs over contiguous tile chunks fed by 1-D TMA
-//   bulk copies (cp.async.bulk + mbarrier, 3 stages) -- slower in steady state.
+//   - p2p: the slot holds stamped entries (tile_encode.cuh) that peers read
+//     over NVLink once the rank's ready flag is up.
+// (A persistent variant fed by 1-D TMA bulk copies and a one-tile variant
+// loading through shared memory by TMA measured slower -- 59.7 and 58.4 us
+// against 51.6 / 55.3 us, DESIGN.md Sec. 6 -- and were removed.)
 // Packing (on demand: NCCL exchange, gtc_message): gtc_group_sums_kernel +
 //   gtc_compact_kernel turn a segmented message (this rank's, or a peer's over
 //   NVLink) into the contiguous wire format.
-// No atomics, no memset, no state carried between calls except the epoch.
+// Atomics: one integer atomicAdd per tile into the step's word counter (order-
+// free), and atomicOr of the sticky non-finite flag.  No state is carried
+// between calls except the epoch and the previous counts in the tags.
 //
 // HBM bytes per parameter (algorithmic): 4 (read g) + 4 (read r) + 4 (write r)
 // + 4*rho (write words); + 8 B per tile (tag).
@@ -46,219 +49,8 @@ namespace gtc {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kStages = 3;                       // TMA pipeline depth per CTA
-constexpr int kTileBytes = kTile * 4;             // 16 KB per tensor per tile
-constexpr int kVec4PerTile = kTile / 4;           // float4 per tensor per tile
 constexpr int kCompactThreads = 256;
-constexpr int kMaxChunkTiles = 2048;              // 2^31 params = 524288 tiles over 256+ chunks
 
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_addr(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 :: "r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    const unsigned a = smem_addr(bar);
-    unsigned done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done) : "r"(a), "r"(parity) : "memory");
-    }
-}
-
-// 1-D bulk copy global -> shared, completion counted on an mbarrier.
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
-                                            unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
-}
-
-template <bool HAS_G>
-struct Smem {
-    float4 r[kStages][kVec4PerTile];
-    float4 g[HAS_G ? kStages : 1][HAS_G ? kVec4PerTile : 1];
-};
-
-// Thread 0: start the TMA copies of `tile` into stage s (full tiles only; the
-// ragged last tile is loaded directly by the consumer).
-template <bool HAS_G>
-__device__ __forceinline__ void issue_stage(const EncodeParams& p, Smem<HAS_G>& sm, unsigned long long* full,
-                                            int s, long long tile) {
-    if (tile >= p.num_tiles) return;
-    const long long base = tile * kTile;
-    if (base + kTile > p.n) return;
-    mbar_arrive_expect_tx(&full[s], HAS_G ? 2u * kTileBytes : (unsigned)kTileBytes);
-    tma_load_1d(sm.r[s], p.r + base, kTileBytes, &full[s]);
-    if (HAS_G) tma_load_1d(sm.g[s], p.g + base, kTileBytes, &full[s]);
-}
-
-template <int CMP, bool HAS_G>
-__global__ void __launch_bounds__(kEncThreads, 2) gtc_encode_tiles_kernel(const EncodeParams p) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem<HAS_G>& sm = *reinterpret_cast<Smem<HAS_G>*>(smem_raw);
-    unsigned* s_cnt = reinterpret_cast<unsigned*>(smem_raw + sizeof(Smem<HAS_G>));  // [chunk_tiles]
-    __shared__ __align__(8) unsigned long long full[kStages];
-    __shared__ unsigned s_scan[kEncVec * kEncWarps];
-    __shared__ unsigned s_total;
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const long long t_begin = (long long)blockIdx.x * p.chunk_tiles;
-    const long long t_end = min(t_begin + p.chunk_tiles, (long long)p.num_tiles);
-
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
-        for (int s = 0; s < kStages; ++s)
-            if (t_begin + s < t_end) issue_stage<HAS_G>(p, sm, full, s, t_begin + s);
-    }
-    __syncthreads();
-    const float tau = p.tau;
-    const unsigned lt = lanemask_lt();
-
-    int it = 0;
-    for (long long tile = t_begin; tile < t_end; ++tile, ++it) {
-        const int s = it % kStages;
-        const long long base = tile * kTile;
-        const bool full_tile = base + kTile <= p.n;
-
-        // ---- load the tile from its stage (or directly, for the ragged tail)
-        float4 rv[kEncVec];
-        float4 gv[kEncVec];
-        if (full_tile) {
-            mbar_wait(&full[s], (unsigned)(it / kStages) & 1u);
-#pragma unroll
-            for (int j = 0; j < kEncVec; ++j) {
-                rv[j] = sm.r[s][j * kEncThreads + tid];
-                if (HAS_G) gv[j] = sm.g[s][j * kEncThreads + tid];
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < kEncVec; ++j) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const long long i = base + (long long)(j * kEncThreads + tid) * 4 + e;
-                    set_comp(rv[j], e, i < p.n ? p.r[i] : 0.0f);
-                    if (HAS_G) set_comp(gv[j], e, i < p.n ? p.g[i] : 0.0f);
-                }
-            }
-        }
-
-        // ---- residual accumulate, threshold, quantize
-        unsigned sel = 0u, neg = 0u;
-        bool nonfinite = false;
-#pragma unroll
-        for (int j = 0; j < kEncVec; ++j) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float v = HAS_G ? __fadd_rn(comp(rv[j], e), comp(gv[j], e)) : comp(rv[j], e);
-                const float a = fabsf(v);
-                nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
-                const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
-                const bool ng = v < 0.0f;
-                const float rn = sl ? (ng ? __fadd_rn(v, tau) : __fsub_rn(v, tau)) : v;
-                set_comp(rv[j], e, rn);
-                sel |= (unsigned)sl << (j * 4 + e);
-                neg |= (unsigned)(sl && ng) << (j * 4 + e);
-            }
-        }
-
-        // ---- write the residual back
-        if (full_tile) {
-            float4* r4 = reinterpret_cast<float4*>(p.r + base);
-#pragma unroll
-            for (int j = 0; j < kEncVec; ++j) st_stream(r4 + j * kEncThreads + tid, rv[j]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < kEncVec; ++j) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const long long i = base + (long long)(j * kEncThreads + tid) * 4 + e;
-                    if (i < p.n) p.r[i] = comp(rv[j], e);
-                }
-            }
-        }
-        if (__any_sync(kFull, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
-
-        // ---- intra-tile ranks
-        unsigned my_off[kEncVec];
-#pragma unroll
-        for (int j = 0; j < kEncVec; ++j) {
-            const unsigned c = __popc((sel >> (4 * j)) & 0xfu);  // 0..4
-            const unsigned b0 = __ballot_sync(kFull, c & 1u);
-            const unsigned b1 = __ballot_sync(kFull, c & 2u);
-            const unsigned b2 = __ballot_sync(kFull, c & 4u);
-            my_off[j] = __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
-            if (lane == 0) s_scan[j * kEncWarps + warp] = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
-        }
-        __syncthreads();  // stage s fully read; s_scan complete
-
-        if (warp == 0) {
-            if (lane == 0 && tile + kStages < t_end)
-                issue_stage<HAS_G>(p, sm, full, s, tile + kStages);  // refill stage s
-            const unsigned x = s_scan[lane];
-            unsigned incl = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += y;
-            }
-            s_scan[lane] = incl - x;
-            if (lane == 31) {
-                s_total = incl;
-                s_cnt[it] = incl;
-                if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);
-                if (tile == 0) *p.k_next = 0ull;
-            }
-        }
-        __syncthreads();  // tile-local offsets known
-
-        // ---- pack and store the words, compacted, in the tile's slot
-        const unsigned total = s_total;
-        if (total != 0) {
-            unsigned* dst = p.seg + base;
-#pragma unroll
-            for (int j = 0; j < kEncVec; ++j) {
-                unsigned o = s_scan[j * kEncWarps + warp] + my_off[j];
-                const unsigned i0 = (unsigned)(base + (long long)(j * kEncThreads + tid) * 4);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if ((sel >> (4 * j + e)) & 1u) {
-                        dst[o] = ((i0 + e) << 1) | ((neg >> (4 * j + e)) & 1u);
-                        ++o;
-                    }
-                }
-            }
-        }
-    }
-    // Publish the chunk's tags after all its words (barrier).
-    __syncthreads();
-    if (tid == 0) {
-        for (long long t = t_begin; t < t_end; ++t) p.tags[t] = make_tag(p.epoch, s_cnt[t - t_begin]);
-    }
-}
-
-// TMA = true: the tile's r (and g) arrive by two 16 KB 1-D bulk copies into
-// shared memory (one mbarrier), so the loads in flight do not occupy
-// registers and more CTAs fit per SM (GTC_ENCODE_VARIANT=tma).
 // fused SGD-momentum apply (world 1, GTC_ACCUM_MOMENTUM; reading M1): for
 // every element, u = fl(c * tau) with c in {-1, 0, +1}, buf = fl(fl(mu * buf) + u),
 // w = fmaf(alpha, buf, w)
@@ -268,17 +60,15 @@ __device__ __forceinline__ void momentum_elem(float& w, float& b, int c, float t
     w = __fmaf_rn(alpha, b, w);
 }
 
-template <int CMP, bool HAS_G, bool TMA, bool MOM>
-__global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_kernel(const EncodeParams p) {
+template <int CMP, bool HAS_G, bool MOM>
+__global__ void __launch_bounds__(kTileThreads, 4) gtc_encode_tile_kernel(const EncodeParams p) {
     __shared__ unsigned s_scan[kTileVec * kTileWarps];
     __shared__ unsigned s_total, s_prev;
-    extern __shared__ __align__(128) float4 s_tile[];  // TMA: [r | g] of the tile
-    __shared__ __align__(8) unsigned long long s_bar;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const long long tile = p.tile_begin + (long long)blockIdx.x;
+    const long long tile = blockIdx.x;
     const long long base = tile * kTile;
     const bool full_tile = base + kTile <= p.n;
 
@@ -289,26 +79,14 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
 
+    // p2p: the count of this slot's previous (same-parity) step, whose entries
+    // beyond the new count are cleared (tile_encode.cuh); loaded first so its
+    // latency hides under the tile loads
+    unsigned prev = 0u;
+    if (p.publish_sys && tid == kTileThreads - 1) prev = ld_tag_count(p.tags + tile);
     float4 rv[kTileVec];
     float4 gv[kTileVec];
-    if (full_tile && TMA) {
-        if (tid == 0) {
-            mbar_init(&s_bar, 1);
-            fence_mbar_init();
-            mbar_arrive_expect_tx(&s_bar, HAS_G ? 2u * kTileBytes : (unsigned)kTileBytes);
-            tma_load_1d(s_tile, p.r + base, kTileBytes, &s_bar);
-            if (HAS_G) tma_load_1d(s_tile + kVec4PerTile, p.g + base, kTileBytes, &s_bar);
-        }
-        __syncthreads();  // the barrier is initialised before anyone waits on it
-        mbar_wait(&s_bar, 0u);
-#pragma unroll
-        for (int j = 0; j < kTileVec; ++j) {
-            rv[j] = s_tile[j * kTileThreads + tid];
-            if (HAS_G) gv[j] = s_tile[kVec4PerTile + j * kTileThreads + tid];
-        }
-    } else {
-        load_tile<HAS_G>(p, base, full_tile, tid, rv, gv);
-    }
+    load_tile<HAS_G>(p, base, full_tile, tid, rv, gv);
 
     const float tau = p.tau;
     unsigned sel, neg;
@@ -345,14 +123,12 @@ __global__ void __launch_bounds__(kTileThreads, TMA ? 5 : 4) gtc_encode_tile_ker
     unsigned my_off[kTileVec];
     tile_scan_ballots(sel, lane, warp, my_off, s_scan);
     __syncthreads();
-    if (warp == 0) {
+    if (warp == kTileWarps - 1) {
         const unsigned incl = tile_scan_finish(lane, s_scan);
         if (lane == 31) {
             s_total = incl;
-            // p2p: the count of this slot's previous (same-parity) step, whose
-            // entries beyond the new count are cleared (tile_encode.cuh)
-            if (p.publish_sys) s_prev = (unsigned)(p.tags[tile] & 0xffffffffull);
-            else p.tags[tile] = make_tag(p.epoch, incl);
+            s_prev = prev;
+            if (!p.publish_sys) p.tags[tile] = make_tag(p.epoch, incl);
             if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);    // integer: order-free
             if (tile == 0) *p.k_next = 0ull;
         }
@@ -514,80 +290,23 @@ __global__ void __launch_bounds__(kCompactThreads) gtc_compact_kernel(const Comp
 }
 
 template <int CMP, bool HAS_G>
-cudaError_t launch_tiles(EncodeParams& p, cudaStream_t s) {
-    static std::once_flag once;
-    static int per_sm = 0, sms = 0;
-    static cudaError_t init_err = cudaSuccess;
-    // + per-tile counts of the chunk (<= kMaxChunkTiles: n < 2^31 over >= 256 chunks)
-    const size_t smem = sizeof(Smem<HAS_G>) + sizeof(unsigned) * kMaxChunkTiles;
-    auto kern = gtc_encode_tiles_kernel<CMP, HAS_G>;
-    std::call_once(once, [&] {
-        init_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (init_err != cudaSuccess) return;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        init_err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (init_err != cudaSuccess) return;
-        init_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEncThreads, smem);
-        if (per_sm < 1) per_sm = 1;
-    });
-    if (init_err != cudaSuccess) return init_err;
-    int grid = sms * per_sm;
-    if (grid > kMaxChunks) grid = kMaxChunks;
-    if (grid > p.num_tiles) grid = p.num_tiles;
-    p.chunk_tiles = (p.num_tiles + grid - 1) / grid;
-    if (p.chunk_tiles > kMaxChunkTiles) p.chunk_tiles = kMaxChunkTiles;
-    p.num_chunks = (p.num_tiles + p.chunk_tiles - 1) / p.chunk_tiles;
-    if (p.num_chunks > kMaxChunks) return cudaErrorInvalidValue;
-    kern<<<p.num_chunks, kEncThreads, smem, s>>>(p);
-    return cudaGetLastError();
-}
-
-// Encode variant: one tile per CTA with register loads (default, 0), the
-// same with a TMA bulk copy into shared memory (GTC_ENCODE_VARIANT=tma, 2), or
-// the persistent TMA pipeline (GTC_ENCODE_VARIANT=persistent, 1); the last
-// two are kept for measurement.
-int encode_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("GTC_ENCODE_VARIANT");
-        v = 0;
-        if (e && std::strcmp(e, "persistent") == 0) v = 1;
-        if (e && std::strcmp(e, "tma") == 0) v = 2;
-    }
-    return v;
-}
-bool use_persistent() { return encode_variant() == 1; }
-
-
-template <int CMP, bool HAS_G>
 cudaError_t launch_tile(EncodeParams& p, cudaStream_t s) {
-    p.chunk_tiles = 1;
-    p.num_chunks = p.num_tiles;
-    if (p.tile_end <= p.tile_begin) return cudaSuccess;
-    const bool tma = encode_variant() == 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(p.tile_end - p.tile_begin));
+    cfg.gridDim = dim3((unsigned)p.num_tiles);
     cfg.blockDim = dim3(kTileThreads);
-    cfg.dynamicSmemBytes = tma ? (HAS_G ? 2 : 1) * (size_t)kTileBytes : 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (p.target && p.accum_mode == GTC_ACCUM_MOMENTUM) {
-        cfg.dynamicSmemBytes = 0;
-        return cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, false, true>, p);
-    }
-    return tma ? cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, true, false>, p)
-               : cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, false, false>, p);
+    if (p.target && p.accum_mode == GTC_ACCUM_MOMENTUM)
+        return cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, true>, p);
+    return cudaLaunchKernelEx(&cfg, gtc_encode_tile_kernel<CMP, HAS_G, false>, p);
 }
 
 template <int CMP>
 cudaError_t launch_cmp(EncodeParams& p, cudaStream_t s) {
-    if (use_persistent() && !p.target && !p.publish_sys && p.tile_begin == 0 && p.tile_end == p.num_tiles)
-        return p.g ? launch_tiles<CMP, true>(p, s) : launch_tiles<CMP, false>(p, s);
     return p.g ? launch_tile<CMP, true>(p, s) : launch_tile<CMP, false>(p, s);
 }
 
@@ -608,17 +327,19 @@ cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s) {
     return cmp_mode == GTC_CMP_GE ? launch_cmp<GTC_CMP_GE>(p, s) : launch_cmp<GTC_CMP_GT>(p, s);
 }
 
-// p2p: launched right after the encode kernel on the same stream.  The kernel
-// boundary orders every encode store before this kernel; one system-scope
-// fence then makes them visible to the peers and the release store raises
-// this rank's ready flag, which peers acquire before reading over NVLink.
-__global__ void gtc_publish_kernel(Ctrl* ctrl, int slot, unsigned long long step) {
+// p2p loopback group (gtc_exchange): launched after the encode kernel on the
+// same stream.  The kernel boundary orders every encode store before this
+// kernel; one system-scope fence then makes them visible to the peers and the
+// release store raises this rank's ready flag, which peers acquire before
+// reading.  (Across processes the decode kernel's block 0 does the same at
+// its start, saving this launch.)
+__global__ void gtc_publish_kernel(Ctrl* ctrl, unsigned long long step) {
     __threadfence_system();
-    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&ctrl->ready[slot]), "l"(step) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&ctrl->ready), "l"(step) : "memory");
 }
 
-cudaError_t launch_publish(Ctrl* ctrl, int slot, unsigned long long step, cudaStream_t s) {
-    gtc_publish_kernel<<<1, 1, 0, s>>>(ctrl, slot, step);
+cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s) {
+    gtc_publish_kernel<<<1, 1, 0, s>>>(ctrl, step);
     return cudaGetLastError();
 }
 

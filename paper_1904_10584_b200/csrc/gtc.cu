@@ -17,7 +17,9 @@
 //        ncclAllGather of the words and tile offsets.
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -48,18 +50,20 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 //   recv_off  i32[world * (T + 1)]               nccl: all-gathered tile offsets
 //   sim_off   i32[max_sim_msgs * (T + 1)]        tile offsets for decode_apply_msgs
 //   push[p][m] T records of kPushRec bytes        p2p: what rank m pushed (fused step), p < 2
+//   group     FusedStepParams[world]             loopback: the group launch's parameters
 struct Layout {
     int nseg;
     size_t ctrl, group_sum, seg_tags[2], seg_words[2];
     size_t msg_hdr, msg_off, msg_words;
     size_t ipc, kx_all, recv, recv_off, sim_off;
     size_t push, push_slot;  // push[p][m] at push + (p * world + m) * push_slot
+    size_t group;
     size_t total;
 };
 
 constexpr size_t kIpcRecord = kIpcRecordBytes;
 
-Layout make_layout(long long n, int world, bool p2p, long long capacity, int max_sim_msgs) {
+Layout make_layout(long long n, int world, bool p2p, bool loopback, long long capacity, int max_sim_msgs) {
     const long long tiles = (n + kTile - 1) / kTile;
     const size_t T = (size_t)std::max(tiles, 1LL);
     Layout L{};
@@ -89,7 +93,11 @@ Layout make_layout(long long n, int world, bool p2p, long long capacity, int max
     L.push = L.push_slot = 0;
     if (world > 1 && p2p) {
         L.push_slot = align_up((size_t)kPushRec * T, 256);
-        L.push = o;  o += 2 * (size_t)world * L.push_slot;
+        L.push = o;  o = align_up(o + 2 * (size_t)world * L.push_slot, 256);
+    }
+    L.group = 0;
+    if (loopback) {
+        L.group = o; o = align_up(o + sizeof(FusedStepParams) * (size_t)world, 256);
     }
     L.total = o;
     return L;
@@ -104,6 +112,10 @@ struct gtc_ctx {
     int rank = 0, world = 1, device = 0;
     int cmp_mode = GTC_CMP_GT;
     bool p2p = false;
+    bool loopback = false;          // GTC_LOOPBACK: a rank of an in-process group (no NCCL, no IPC)
+    bool connected = false;         // loopback: gtc_connect_loopback done
+    bool dead = false;              // the NCCL communicator was aborted (timeout)
+    unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;  // p2p: longest wait for a peer
     bool split_step = false;        // GTC_STEP_SPLIT: gtc_step as encode + decode_apply kernels
     int num_tiles = 0;
     ncclComm_t comm = nullptr;
@@ -127,9 +139,7 @@ struct gtc_ctx {
     unsigned long long encodes = 0; // encodes since bind (the step value of the p2p ready flags)
     float* mom_buf = nullptr;       // GTC_ACCUM_MOMENTUM state (gtc_bind_momentum)
     float mom_mu = 0.f;
-    cudaStream_t side = nullptr;    // p2p gtc_step pipeline: decode chunks run here
-    cudaEvent_t ev_chunk[kMaxPipe] = {};
-    cudaEvent_t ev_join = nullptr;
+    FusedStepParams* host_group = nullptr;  // loopback rank 0: pinned staging of the group parameters
     int packed_rank = -1;           // whose message the contiguous region holds (-1: stale)
     bool push_clean[2] = {true, true};  // p2p: the last step of this parity was fused (or none yet)
 
@@ -188,6 +198,7 @@ unsigned char* rank_ws(const gtc_ctx* c, int rank) {
 }
 
 // p2p: map every peer's workspace (ipc.cu); all ranks agree on the outcome.
+// (Loopback contexts are connected by gtc_connect_loopback instead.)
 gtc_status connect_peers(gtc_ctx* c) {
     const IpcResult r = ipc_map_peers(c->comm, c->rank, c->world, c->ws, c->L.total, c->ws + c->L.ipc, c->peer_ws,
                                       c->peer_alloc);
@@ -271,8 +282,15 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     if (!(tau > 0.f) || std::isinf(tau)) return GTC_EINVAL;
     if (world < 1 || rank < 0 || rank >= world) return GTC_EINVAL;
     if (world > GTC_MAX_MSGS) return GTC_EUNSUPPORTED;
-    if (flags & ~(uint32_t)(GTC_CMP_GE | GTC_EXCHANGE_NCCL | GTC_STEP_SPLIT)) return GTC_EINVAL;
-    if ((world > 1) != (nccl_unique_id != nullptr)) return GTC_EINVAL;
+    if (flags & ~(uint32_t)(GTC_CMP_GE | GTC_EXCHANGE_NCCL | GTC_STEP_SPLIT | GTC_LOOPBACK)) return GTC_EINVAL;
+    const bool loopback = (flags & GTC_LOOPBACK) != 0;
+    if (loopback) {
+        // an in-process group: no NCCL id, p2p exchange only
+        if (nccl_unique_id != nullptr || (flags & GTC_EXCHANGE_NCCL) || world < 2) return GTC_EINVAL;
+        if (world > kFusedMaxRanks) return GTC_EUNSUPPORTED;
+    } else if ((world > 1) != (nccl_unique_id != nullptr)) {
+        return GTC_EINVAL;
+    }
 
     gtc_ctx* c = new (std::nothrow) gtc_ctx();
     if (!c) return GTC_EINVAL;
@@ -283,7 +301,12 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     c->device = cuda_device;
     c->cmp_mode = (int)(flags & GTC_CMP_GE);
     c->p2p = world > 1 && !(flags & GTC_EXCHANGE_NCCL);
+    c->loopback = loopback;
     c->split_step = (flags & GTC_STEP_SPLIT) != 0;
+    if (const char* e = std::getenv("GTC_PEER_TIMEOUT_MS")) {
+        const long long ms = std::atoll(e);
+        if (ms > 0) c->timeout_ns = (unsigned long long)ms * 1000000ull;
+    }
     c->num_tiles = (int)((n_params + kTile - 1) / kTile);
     c->last_k.assign(world, 0);
 
@@ -294,7 +317,16 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
         delete c;
         return GTC_ECUDA;
     }
-    if (world > 1) {
+    if (loopback && rank == 0) {
+        e = cudaHostAlloc(reinterpret_cast<void**>(&c->host_group), sizeof(FusedStepParams) * kFusedMaxRanks,
+                          cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+            cudaFreeHost(c->host_kx);
+            delete c;
+            return GTC_ECUDA;
+        }
+    }
+    if (world > 1 && !loopback) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_unique_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
@@ -313,7 +345,7 @@ gtc_status gtc_workspace_size(const gtc_ctx* c, int64_t max_words_per_rank, int 
     if (!c || !bytes) return GTC_EINVAL;
     if (max_sim_msgs < 0 || max_sim_msgs > GTC_MAX_MSGS) return GTC_EINVAL;
     const long long cap = max_words_per_rank <= 0 ? c->n : std::min<long long>(max_words_per_rank, c->n);
-    *bytes = make_layout(c->n, c->world, c->p2p, cap, max_sim_msgs).total;
+    *bytes = make_layout(c->n, c->world, c->p2p, c->loopback, cap, max_sim_msgs).total;
     return GTC_OK;
 }
 
@@ -324,7 +356,7 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     if (reinterpret_cast<uintptr_t>(dev_ptr) & 255u) return fail(c, GTC_EALIGN, "workspace not 256-byte aligned");
     if (max_sim_msgs < 0 || max_sim_msgs > GTC_MAX_MSGS) return fail(c, GTC_EINVAL, "max_sim_msgs");
     const long long cap = max_words_per_rank <= 0 ? c->n : std::min<long long>(max_words_per_rank, c->n);
-    const Layout L = make_layout(c->n, c->world, c->p2p, cap, max_sim_msgs);
+    const Layout L = make_layout(c->n, c->world, c->p2p, c->loopback, cap, max_sim_msgs);
     if (bytes < L.total) return fail(c, GTC_EINVAL, "workspace too small");
     DeviceGuard g(c->device);
     unsigned char* b = static_cast<unsigned char*>(dev_ptr);
@@ -352,7 +384,7 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
         c->recv_off = reinterpret_cast<int*>(b + L.recv_off);
     }
     c->sim_off = reinterpret_cast<int*>(b + L.sim_off);
-    if (c->world > 1 && c->p2p) {
+    if (c->world > 1 && c->p2p && !c->loopback) {
         gtc_status s = connect_peers(c);
         if (s != GTC_OK) {
             c->ws = nullptr;
@@ -368,6 +400,8 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
 
 static gtc_status check_encode_args(gtc_ctx* c, const float* grad, float* residual) {
     if (!c->bound) return fail(c, GTC_ESTATE, "encode: workspace not bound");
+    if (c->dead) return fail(c, GTC_ESTATE, "the NCCL communicator was aborted after a timeout");
+    if (c->loopback && !c->connected) return fail(c, GTC_ESTATE, "loopback: call gtc_connect_loopback first");
     if (c->n > 0 && !residual) return fail(c, GTC_EINVAL, "encode: residual is null");
     if (!aligned16(residual) || !aligned16(grad)) return fail(c, GTC_EALIGN, "encode: grad/residual alignment");
     return GTC_OK;
@@ -380,10 +414,9 @@ static void begin_step(gtc_ctx* c) {
     c->packed_rank = -1;
 }
 
-// Encode tiles [tb, te) of the current step on `stream`; p2p: then publish
-// them under ready slot `slot` (-1: no publish).
-static gtc_status encode_range(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream,
-                               float* fused_target, float fused_alpha, int fused_mode, int tb, int te, int slot) {
+// Encode every tile of the current step on `stream`.
+static gtc_status encode_launch(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream,
+                                float* fused_target, float fused_alpha, int fused_mode) {
     const int par = seg_parity(c);
     EncodeParams p{};
     p.g = grad;
@@ -404,17 +437,10 @@ static gtc_status encode_range(gtc_ctx* c, const float* grad, float* residual, c
     p.publish_sys = (c->world > 1 && c->p2p) ? 1 : 0;
     if (p.publish_sys) c->push_clean[par] = false;  // this parity's push records are not maintained
     p.num_tiles = c->num_tiles;
-    p.tile_begin = tb;
-    p.tile_end = te;
     p.step = c->encodes;
     cudaError_t e = launch_encode(p, c->cmp_mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "encode: launch");
     c->launches += 1;
-    if (slot >= 0) {
-        e = launch_publish(c->ctrl, slot, p.step, stream);
-        if (e != cudaSuccess) return cuda_fail(c, e, "encode: publish");
-        c->launches += 1;
-    }
     return GTC_OK;
 }
 
@@ -431,8 +457,8 @@ static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cu
         c->stage = Stage::kEncoded;
         return GTC_OK;
     }
-    // p2p: the decode kernel raises ready[0] when it starts (no publish launch)
-    s = encode_range(c, grad, residual, stream, fused_target, fused_alpha, fused_mode, 0, c->num_tiles, -1);
+    // p2p: the decode kernel raises ready when it starts (no publish launch)
+    s = encode_launch(c, grad, residual, stream, fused_target, fused_alpha, fused_mode);
     if (s != GTC_OK) return s;
     c->stage = Stage::kEncoded;
     return GTC_OK;
@@ -455,7 +481,11 @@ static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
     // Flags are reported now; clear the local copy (stream-ordered after the gather).
     e = cudaMemsetAsync(&c->ctrl->flags, 0, sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "exchange: flag clear");
-    // 2. the one host wait of the step; poll NCCL for asynchronous errors meanwhile.
+    // 2. the one host wait of the step; poll NCCL for asynchronous errors
+    //    meanwhile, and give up after the peer timeout: a rank that never
+    //    joins the all-gather would otherwise hang this one forever.  The
+    //    communicator is aborted (ncclCommAbort) and the context is dead.
+    const auto t_wait = std::chrono::steady_clock::now();
     while (true) {
         e = cudaStreamQuery(stream);
         if (e == cudaSuccess) break;
@@ -463,6 +493,15 @@ static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
         ncclResult_t ar = ncclSuccess;
         if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess)
             return nccl_fail(c, ar, "exchange: async");
+        const auto waited = std::chrono::steady_clock::now() - t_wait;
+        if ((unsigned long long)std::chrono::duration_cast<std::chrono::nanoseconds>(waited).count() > c->timeout_ns) {
+            ncclCommAbort(c->comm);
+            c->comm = nullptr;
+            c->dead = true;
+            c->stage = Stage::kBound;
+            return fail(c, GTC_EPEER, "exchange: a peer did not join the all-gather in time (communicator aborted)");
+        }
+        std::this_thread::yield();
     }
     unsigned long long any_flags = 0;
     long long max_k = 0;
@@ -494,9 +533,17 @@ gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
     if (!c) return GTC_EINVAL;
     if (c->stage != Stage::kEncoded) return fail(c, GTC_ESTATE, "exchange: no encode since the last exchange");
     if (c->world == 1 || c->p2p) {
-        // world 1: nothing to send.  p2p: the encode kernel already published
-        // every tile (epoch-stamped tags); decode_apply reads the peers'
-        // tiles in place over NVLink as they become ready.
+        // world 1: nothing to send.  p2p: decode_apply raises this rank's
+        // ready flag when it starts and reads the peers' tiles in place over
+        // NVLink once theirs are up.  Loopback group: every rank's decode is
+        // queued behind every rank's encode, so the flag goes up here (one
+        // one-thread kernel) -- no kernel ever waits on one not yet running.
+        if (c->loopback) {
+            DeviceGuard g(c->device);
+            const cudaError_t e = launch_publish(c->ctrl, c->encodes, stream);
+            if (e != cudaSuccess) return cuda_fail(c, e, "exchange: publish");
+            c->launches += 1;
+        }
         c->stage = Stage::kExchanged;
         return GTC_OK;
     }
@@ -523,10 +570,10 @@ gtc_status gtc_bind_momentum(gtc_ctx* c, float* buf, float mu) {
     return GTC_OK;
 }
 
-// Decode + apply tiles [tb, te) of the current step on `stream` (p2p: waiting
-// on ready slot `slot` of every peer).
-static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
-                               cudaStream_t stream, int tb, int te, int slot, bool publish) {
+// Decode + apply every tile of the current step on `stream` (p2p: waiting on
+// every rank's ready flag).
+static gtc_status decode_launch(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
+                                cudaStream_t stream) {
     DecodeParams p{};
     if (c->world == 1 || c->p2p) {
         const int par = seg_parity(c);
@@ -540,9 +587,13 @@ static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode,
         p.epoch = c->epoch;
         p.step = c->encodes;
         p.wait = c->world > 1 ? 1 : 0;
-        for (int i = 0; i < c->world && p.wait; ++i)
-            p.ready[i] = &reinterpret_cast<Ctrl*>(rank_ws(c, i) + c->L.ctrl)->ready[slot];
-        if (p.wait && publish) p.publish = &c->ctrl->ready[slot];
+        for (int i = 0; i < c->world && p.wait; ++i) {
+            Ctrl* ci = reinterpret_cast<Ctrl*>(rank_ws(c, i) + c->L.ctrl);
+            p.ready[i] = &ci->ready;
+            p.peer_flags[i] = &ci->flags;
+        }
+        if (p.wait) p.publish = &c->ctrl->ready;
+        p.timeout_ns = c->timeout_ns;
     } else {
         p.segmented = 0;
         for (int i = 0; i < c->world; ++i) {
@@ -553,8 +604,6 @@ static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode,
     p.nmsg = c->world;
     p.n = c->n;
     p.num_tiles = c->num_tiles;
-    p.tile_begin = tb;
-    p.tile_end = te;
     p.tau = c->tau;
     p.alpha = alpha;
     p.target = target;
@@ -565,7 +614,7 @@ static gtc_status decode_range(gtc_ctx* c, float* target, float alpha, int mode,
     p.trace = decode_trace_enabled() ? 1 : 0;
     cudaError_t e = launch_decode_apply(p, mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "decode_apply: launch");
-    if (te > tb) c->launches += 1;
+    if (c->num_tiles > 0) c->launches += 1;
     return GTC_OK;
 }
 
@@ -576,55 +625,8 @@ gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, in
     gtc_status s = check_apply_args(c, target, mode);
     if (s != GTC_OK) return s;
     DeviceGuard g(c->device);
-    s = decode_range(c, target, alpha, mode, counts_out, stream, 0, c->num_tiles, 0, true);
+    s = decode_launch(c, target, alpha, mode, counts_out, stream);
     if (s != GTC_OK) return s;
-    c->stage = Stage::kBound;
-    return GTC_OK;
-}
-
-static int pipeline_chunks(const gtc_ctx* c) {
-    static int k = -1;
-    if (k < 0) {
-        // measured (lstm_am, 1000 steps): K=1 558 / 881 G params/s at N=2 / 4,
-        // K=2 515 / 911, K=4 398 / 720 -- off by default
-        const char* e = std::getenv("GTC_PIPELINE_CHUNKS");
-        k = e ? std::atoi(e) : 1;
-        if (k < 1) k = 1;
-        if (k > kMaxPipe) k = kMaxPipe;
-    }
-    return std::min(k, std::max(c->num_tiles, 1));
-}
-
-// p2p, world > 1: the step as K chunks of tiles.  Chunk i's encode and its
-// ready flag go on the caller's stream; chunk i's decode goes on the side
-// stream after an event on that flag, so the decode's NVLink reads and
-// scattered target updates overlap the encode of the next chunks.  The
-// caller's stream joins the side stream at the end.
-static gtc_status step_pipelined(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
-                                 int mode, cudaStream_t stream, int K) {
-    cudaError_t e = cudaSuccess;
-    if (!c->side) {
-        e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-        for (int i = 0; i < kMaxPipe && e == cudaSuccess; ++i)
-            e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-        if (e != cudaSuccess) return cuda_fail(c, e, "step: pipeline setup");
-    }
-    begin_step(c);
-    const int T = c->num_tiles;
-    for (int i = 0; i < K; ++i) {
-        const int tb = (int)((long long)T * i / K), te = (int)((long long)T * (i + 1) / K);
-        gtc_status s = encode_range(c, grad, residual, stream, nullptr, 0.f, GTC_ACCUM_WEIGHTS, tb, te, i);
-        if (s != GTC_OK) return s;
-        e = cudaEventRecord(c->ev_chunk[i], stream);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_chunk[i], 0);
-        if (e != cudaSuccess) return cuda_fail(c, e, "step: chunk event");
-        s = decode_range(c, target, alpha, mode, nullptr, c->side, tb, te, i, false);
-        if (s != GTC_OK) return s;
-    }
-    e = cudaEventRecord(c->ev_join, c->side);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c->ev_join, 0);
-    if (e != cudaSuccess) return cuda_fail(c, e, "step: join");
     c->stage = Stage::kBound;
     return GTC_OK;
 }
@@ -639,11 +641,14 @@ static bool fused_step_enabled() {
     return v == 1;
 }
 
-static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
-                                 int mode, cudaStream_t stream) {
+// The fused one-kernel step's parameters of rank c (begins the step: epoch,
+// parity); clears this rank's push records on the peers first if the last
+// step of this parity was not fused.
+static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
+                             cudaStream_t stream, int ranks_per_device, FusedStepParams& f) {
     begin_step(c);
     const int par = seg_parity(c);
-    FusedStepParams f{};
+    f = FusedStepParams{};
     EncodeParams& p = f.enc;
     p.g = grad;
     p.r = residual;
@@ -659,13 +664,12 @@ static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual,
     p.mu = c->mom_mu;
     p.publish_sys = 1;
     p.num_tiles = c->num_tiles;
-    p.tile_begin = 0;
-    p.tile_end = c->num_tiles;
     p.step = c->encodes;
     for (int i = 0; i < c->world; ++i) {
         unsigned char* b = rank_ws(c, i);
         f.seg[i] = reinterpret_cast<const unsigned*>(b + c->L.seg_words[par]);
         f.tags[i] = reinterpret_cast<const unsigned long long*>(b + c->L.seg_tags[par]);
+        f.peer_flags[i] = &reinterpret_cast<Ctrl*>(b + c->L.ctrl)->flags;
         f.push_out[i] = nullptr;
         f.push_in[i] = nullptr;
         if (i == c->rank) continue;
@@ -683,11 +687,21 @@ static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual,
     c->push_clean[par] = true;
     f.rank = c->rank;
     f.nranks = c->world;
-    f.lag_groups = step_p2p_lag_groups(c->num_tiles);
+    f.lag_groups = step_p2p_lag_groups(c->num_tiles, ranks_per_device);
+    f.num_groups = (c->num_tiles + kDecGroup - 1) / kDecGroup;
     f.target = target;
     f.alpha = alpha;
     f.flags = &c->ctrl->flags;
+    f.timeout_ns = c->timeout_ns;
     f.trace = decode_trace_enabled() ? 1 : 0;
+    return GTC_OK;
+}
+
+static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
+                                 int mode, cudaStream_t stream) {
+    FusedStepParams f;
+    gtc_status s = fill_fused(c, grad, residual, target, alpha, stream, 1, f);
+    if (s != GTC_OK) return s;
     cudaError_t e = launch_step_p2p(f, c->cmp_mode, mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "step: fused p2p launch");
     c->launches += 1;
@@ -712,22 +726,18 @@ gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* targe
         c->stage = Stage::kBound;
         return GTC_OK;
     }
-    if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1) {
-        const int K = pipeline_chunks(c);
-        if (K == 1 && !c->split_step && fused_step_enabled() && c->world <= kFusedMaxRanks) {
-            gtc_status s = check_encode_args(c, grad, residual);
-            if (s == GTC_OK) s = check_apply_args(c, target, mode);
-            if (s != GTC_OK) return s;
-            DeviceGuard g(c->device);
-            return step_fused_p2p(c, grad, residual, target, alpha, mode, stream);
-        }
-        if (K > 1) {
-            gtc_status s = check_encode_args(c, grad, residual);
-            if (s == GTC_OK) s = check_apply_args(c, target, mode);
-            if (s != GTC_OK) return s;
-            DeviceGuard g(c->device);
-            return step_pipelined(c, grad, residual, target, alpha, mode, stream, K);
-        }
+    if (c && c->loopback)
+        // one rank's whole step would wait on ranks whose encode is not yet
+        // queued: a loopback group steps with gtc_step_group, or with every
+        // rank's encode, then exchange, then decode_apply
+        return fail(c, GTC_EUNSUPPORTED, "step: loopback contexts step with gtc_step_group");
+    if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1 && !c->split_step && fused_step_enabled() &&
+        c->world <= kFusedMaxRanks) {
+        gtc_status s = check_encode_args(c, grad, residual);
+        if (s == GTC_OK) s = check_apply_args(c, target, mode);
+        if (s != GTC_OK) return s;
+        DeviceGuard g(c->device);
+        return step_fused_p2p(c, grad, residual, target, alpha, mode, stream);
     }
     gtc_status s = gtc_encode(c, grad, residual, stream);
     if (s != GTC_OK) return s;
@@ -735,6 +745,80 @@ gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* targe
     if (sx != GTC_OK && sx != GTC_ENONFINITE) return sx;
     s = gtc_decode_apply(c, target, alpha, mode, nullptr, stream);
     return s != GTC_OK ? s : sx;
+}
+
+gtc_status gtc_connect_loopback(gtc_ctx* const* ctxs, int world) {
+    if (!ctxs || world < 2 || world > kFusedMaxRanks) return GTC_EINVAL;
+    for (int r = 0; r < world; ++r) {
+        gtc_ctx* c = ctxs[r];
+        if (!c || !c->loopback || c->world != world || c->rank != r) return fail(c, GTC_EINVAL, "loopback: ranks");
+        if (!c->bound) return fail(c, GTC_ESTATE, "loopback: bind every workspace first");
+        if (c->n != ctxs[0]->n || c->tau != ctxs[0]->tau || c->cmp_mode != ctxs[0]->cmp_mode ||
+            c->L.total != ctxs[0]->L.total)
+            return fail(c, GTC_EINVAL, "loopback: every rank needs the same n, tau, flags and workspace sizes");
+    }
+    // peers on other devices of this process: their memory must be mapped
+    for (int r = 0; r < world; ++r) {
+        for (int m = 0; m < world; ++m) {
+            if (ctxs[m]->device == ctxs[r]->device) continue;
+            DeviceGuard g(ctxs[r]->device);
+            cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[m]->device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+            } else if (e != cudaSuccess) {
+                return cuda_fail(ctxs[r], e, "loopback: cudaDeviceEnablePeerAccess");
+            }
+        }
+    }
+    for (int r = 0; r < world; ++r) {
+        gtc_ctx* c = ctxs[r];
+        c->peer_ws.assign(world, nullptr);
+        for (int m = 0; m < world; ++m) c->peer_ws[m] = ctxs[m]->ws;
+        c->peer_alloc.assign(world, nullptr);
+        c->connected = true;
+    }
+    return GTC_OK;
+}
+
+gtc_status gtc_step_group(gtc_ctx* const* ctxs, int world, const float* const* grads, float* const* residuals,
+                          float* const* targets, float alpha, int mode, uint32_t debug_flags, cudaStream_t stream) {
+    if (!ctxs || world < 2 || world > kFusedMaxRanks || !residuals || !targets) return GTC_EINVAL;
+    gtc_ctx* c0 = ctxs[0];
+    if (!c0 || !c0->host_group) return fail(c0, GTC_EINVAL, "step_group: ctxs[0] is not rank 0 of a loopback group");
+    if (debug_flags >> kFusedMaxRanks) return fail(c0, GTC_EINVAL, "step_group: debug_flags");
+    for (int r = 0; r < world; ++r) {
+        gtc_ctx* c = ctxs[r];
+        if (!c || !c->loopback || c->rank != r || c->world != world) return fail(c0, GTC_EINVAL, "step_group: ranks");
+        if (c->device != c0->device) return fail(c, GTC_EUNSUPPORTED, "step_group: every rank on one device");
+        const float* g = grads ? grads[r] : nullptr;
+        if ((g == nullptr) != (grads == nullptr || grads[0] == nullptr))
+            return fail(c, GTC_EINVAL, "step_group: grads on every rank or on none");
+        gtc_status s = check_encode_args(c, g, residuals[r]);
+        if (s == GTC_OK) s = check_apply_args(c, targets[r], mode);
+        if (s != GTC_OK) return s;
+    }
+    if (c0->num_tiles == 0) return GTC_OK;
+    DeviceGuard guard(c0->device);
+    // the previous launch must be done reading the staging buffer
+    cudaError_t e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_fail(c0, e, "step_group: sync");
+    for (int r = 0; r < world; ++r) {
+        gtc_ctx* c = ctxs[r];
+        gtc_status s = fill_fused(c, grads ? grads[r] : nullptr, residuals[r], targets[r], alpha, stream, world,
+                                  c0->host_group[r]);
+        if (s != GTC_OK) return s;
+        c0->host_group[r].skip = (int)((debug_flags >> r) & 1u);
+    }
+    FusedStepParams* dev = reinterpret_cast<FusedStepParams*>(c0->ws + c0->L.group);
+    e = cudaMemcpyAsync(dev, c0->host_group, sizeof(FusedStepParams) * world, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(c0, e, "step_group: parameters");
+    e = launch_step_p2p_group(dev, c0->host_group[0], world, c0->cmp_mode, mode, stream);
+    if (e != cudaSuccess) return cuda_fail(c0, e, "step_group: launch");
+    for (int r = 0; r < world; ++r) {
+        ctxs[r]->launches += 1;
+        ctxs[r]->stage = Stage::kBound;
+    }
+    return GTC_OK;
 }
 
 gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const int64_t* counts, int nmsg,
@@ -776,8 +860,6 @@ gtc_status gtc_decode_apply_msgs(gtc_ctx* c, const uint32_t* const* msgs, const 
     p.nmsg = nmsg;
     p.n = c->n;
     p.num_tiles = c->num_tiles;
-    p.tile_begin = 0;
-    p.tile_end = c->num_tiles;
     p.tau = c->tau;
     p.alpha = alpha;
     p.target = target;
@@ -916,26 +998,31 @@ gtc_status gtc_debug_step_trace(uint64_t* host, int max_entries) {
                                                                                                 : GTC_ECUDA;
 }
 
-void gtc_destroy(gtc_ctx* c) {
-    if (!c) return;
+gtc_status gtc_quiesce(gtc_ctx* c) {
+    if (!c) return GTC_EINVAL;
     DeviceGuard g(c->device);
-    if (c->world > 1) cudaDeviceSynchronize();
-    if (c->bound && c->p2p && c->comm) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "quiesce: sync");
+    if (c->bound && c->p2p && c->comm && !c->dead) {
         // barrier: no peer may still be reading this rank's workspace (and
         // this rank is done with theirs) when the mappings go away
         int* d = reinterpret_cast<int*>(c->ws + c->L.ipc);
-        if (ncclAllReduce(d, d, 1, ncclInt32, ncclSum, c->comm, 0) == ncclSuccess) cudaStreamSynchronize(0);
+        ncclResult_t r = ncclAllReduce(d, d, 1, ncclInt32, ncclSum, c->comm, 0);
+        if (r != ncclSuccess) return nccl_fail(c, r, "quiesce: barrier");
+        e = cudaStreamSynchronize(0);
+        if (e != cudaSuccess) return cuda_fail(c, e, "quiesce: barrier wait");
     }
-    if (c->side) {
-        cudaStreamSynchronize(c->side);
-        for (int i = 0; i < kMaxPipe; ++i)
-            if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
-        if (c->ev_join) cudaEventDestroy(c->ev_join);
-        cudaStreamDestroy(c->side);
-    }
+    return GTC_OK;
+}
+
+void gtc_destroy(gtc_ctx* c) {
+    if (!c) return;
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
     ipc_unmap(c->peer_alloc);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->host_kx) cudaFreeHost(c->host_kx);
+    if (c->host_group) cudaFreeHost(c->host_group);
     delete c;
 }
 

@@ -14,12 +14,8 @@
 namespace gtc {
 
 constexpr int kTile = GTC_TILE;                        // parameters per tile
-constexpr int kEncThreads = 512;                       // encode CTA size
-constexpr int kEncWarps = kEncThreads / 32;
-constexpr int kEncVec = kTile / (kEncThreads * 4);     // float4 per thread per tensor
 constexpr int kDecThreads = 256;                       // decode_apply CTA size
 constexpr int kDecMaxTilesPerCta = 8;                  // <= 32 KB of int8 counts per CTA
-static_assert(kEncVec * kEncWarps == 32, "block scan assumes one (round, warp) entry per lane");
 static_assert(kTile == kDecThreads * 16, "decode sweep assumes 16 counts per thread");
 
 // Sticky device flags (Ctrl::flags).
@@ -27,7 +23,8 @@ enum : unsigned long long {
     kFlagNonFinite = 1ull,  // a residual element was NaN/Inf
     kFlagCapacity = 2ull,   // a contiguous message did not fit max_words_per_rank
     kFlagCorrupt = 4ull,    // a caller-supplied message was not canonical
-    kFlagPeer = 8ull,       // a peer did not publish a tile in time (p2p exchange)
+    kFlagPeer = 8ull,       // a peer did not publish in time (p2p exchange); raised on
+                            // EVERY rank's flags by the rank that timed out
 };
 
 // Control block at the start of the workspace.  k and flags are adjacent so
@@ -35,10 +32,12 @@ enum : unsigned long long {
 struct alignas(256) Ctrl {
     unsigned long long k_acc[2];  // words of the encode of step parity p (accumulated per tile)
     unsigned long long flags;     // sticky flags
-    unsigned long long ready[8];  // p2p: per pipeline chunk, the step (encodes since bind)
-                                  // whose message the rank has published
+    unsigned long long ready;     // p2p: the step (encodes since bind) whose message the
+                                  // rank has published (separate calls)
+    unsigned long long counted;   // p2p sharded decode: the step whose owner counts the
+                                  // rank has published (Sec. f4)
+    unsigned long long arrive[2]; // p2p sharded decode: CTA arrival counters per parity
 };
-constexpr int kMaxPipe = 8;       // most pipeline chunks of gtc_step (p2p)
 
 // Header of a contiguous message region.
 struct MsgHeader {
@@ -54,10 +53,10 @@ struct MsgHeader {
 // tile-local entries instead (tile_encode.cuh: stamp(epoch) << 13 | local << 1
 // | neg), so a reader can tell this step's entries from older ones without a
 // writer-side fence.  The separate calls publish the whole message by raising
-// Ctrl::ready[slot] = step after a system-scope fence -- done by block 0 of the
-// decode kernel (stream order puts every encode store before it), or by a
-// one-thread publish kernel per chunk in the pipelined gtc_step -- and peers
-// acquire that flag before reading over NVLink; the fused step
+// Ctrl::ready = step after a system-scope fence -- done by block 0 of the
+// decode kernel (stream order puts every encode store before it), or, in a
+// loopback group, by the one-thread publish kernel gtc_exchange launches --
+// and peers acquire that flag before reading over NVLink; the fused step
 // (step_p2p.cu) instead pushes per-tile records and checks stamps.  Decode
 // reads exactly the words of the tiles it owns, from every rank, without a
 // global prefix scan.
@@ -87,13 +86,7 @@ struct EncodeParams {
     int publish_sys;               // p2p: peers read this message over NVLink
     unsigned long long step;       // p2p: encodes since bind (the value raised in Ctrl::ready)
     int num_tiles;
-    int tile_begin, tile_end;      // the tiles this launch encodes (pipeline chunk)
-    int chunk_tiles;               // persistent variant: tiles per CTA (set by launch_encode)
-    int num_chunks;                // persistent variant: grid (set by launch_encode)
 };
-
-// Most persistent-encode CTAs (chunks) a launch may use.
-constexpr int kMaxChunks = 1024;
 // Packing a segmented message first sums the counts of groups of kGroupTiles tiles.
 constexpr int kGroupTiles = 64;
 
@@ -121,11 +114,12 @@ struct DecodeParams {
     unsigned long long step;       // p2p: wait until every rank's Ctrl::ready >= step
     int wait;                      // segmented p2p: acquire every rank's ready flag first
     const unsigned long long* ready[GTC_MAX_MSGS];  // p2p: each rank's Ctrl::ready
+    unsigned long long* peer_flags[GTC_MAX_MSGS];   // p2p: every rank's Ctrl::flags (timeout broadcast)
     unsigned long long* publish;   // p2p: raise this rank's ready flag (= step) first, or null
+    unsigned long long timeout_ns; // p2p: longest wait for a peer
     int nmsg;
     long long n;
     int num_tiles;
-    int tile_begin, tile_end;      // the tiles this launch decodes (pipeline chunk)
     float tau;
     float alpha;
     float* target;
@@ -162,6 +156,9 @@ struct FusedStepParams {
     float* target;
     float alpha;
     unsigned long long* flags;                         // this rank's Ctrl::flags
+    unsigned long long* peer_flags[kFusedMaxRanks];    // every rank's Ctrl::flags (timeout broadcast)
+    unsigned long long timeout_ns;                     // longest wait for a peer's tile
+    int skip;                                          // loopback test hook: this rank does nothing
     int trace;                                         // GTC_DECODE_TRACE=1: phase stamps (debug)
 };
 
@@ -186,11 +183,16 @@ void ipc_unmap(std::vector<void*>& allocs);
 bool pdl_enabled();  // programmatic dependent launch (GTC_PDL=0 disables)
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
-cudaError_t launch_publish(Ctrl* ctrl, int slot, unsigned long long step, cudaStream_t s);
+cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
 cudaError_t launch_step_p2p(FusedStepParams& p, int cmp_mode, int accum_mode, cudaStream_t s);
-int step_p2p_lag_groups(int num_tiles);
+// Loopback group (tests): the fused step of `world` ranks as ONE launch; the
+// per-rank parameters live in device memory (`group`, copied there by the
+// caller); `host` holds the same parameters for the launch configuration.
+cudaError_t launch_step_p2p_group(const FusedStepParams* group, const FusedStepParams& host, int world,
+                                  int cmp_mode, int accum_mode, cudaStream_t s);
+int step_p2p_lag_groups(int num_tiles, int ranks_per_device);
 cudaError_t read_step_trace(unsigned long long* host, int max_entries);
 cudaError_t read_decode_trace(unsigned long long* host, int max_entries);
 bool decode_trace_enabled();

@@ -34,9 +34,13 @@
 // read, and the decode CTAs then only wait on local memory.
 //
 // Progress: a decode CTA waits only for tiles encoded by lower-numbered CTAs
-// of each rank (dispatched earlier, in blockIdx order), whose encodes never
-// wait.  A wait longer than 30 s sets kFlagPeer (GTC_EPEER) and the CTA gives
-// up -- an error, never a hang.
+// of each rank, whose encodes never wait.  HARDWARE ASSUMPTION: the CTAs of a
+// grid are dispatched in increasing blockIdx order (so every CTA waited on has
+// been dispatched; no MPS/green-context partitioning that could starve one).
+// A wait longer than the context's timeout (30 s default) raises kFlagPeer
+// (GTC_EPEER) on EVERY rank and the CTA gives up -- an error, never a hang;
+// the replicas are then inconsistent (the other decode CTAs applied their
+// tiles) and the caller must restore a checkpoint (gtc.h, gtc_check).
 //
 // Buffer reuse: the segmented buffers alternate with the step parity.  A rank
 // overwrites parity p at step e + 2 only after its step e + 1 kernel read
@@ -58,7 +62,6 @@ namespace {
 
 constexpr int kSpecPerThread = 4;   // speculative entry loads per thread (decode CTA)
 constexpr int kApplyBatch = 4;      // target float4 loads per thread before their stores
-constexpr unsigned long long kTimeoutNs = 30ull * 1000 * 1000 * 1000;
 static_assert(kDecGroup * kFusedMaxRanks <= kTileThreads, "one tag poller per (tile, rank)");
 
 // Opt-in phase trace (GTC_DECODE_TRACE=1): thread 0 of each of the first
@@ -116,6 +119,10 @@ __device__ __forceinline__ void encode_cta(const FusedStepParams& f, long long t
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long base = t * kTile;
     const bool full_tile = base + kTile <= p.n;
+    // this slot's previous same-parity count (its entries beyond the new count
+    // are cleared), loaded first so its latency hides under the tile loads
+    unsigned prev_ld = 0u;
+    if (tid == kTileThreads - 1) prev_ld = ld_tag_count(p.tags + t);
     float4 rv[kTileVec], gv[kTileVec];
     load_tile<HAS_G>(p, base, full_tile, tid, rv, gv);
     unsigned sel, neg;
@@ -126,11 +133,11 @@ __device__ __forceinline__ void encode_cta(const FusedStepParams& f, long long t
     unsigned my_off[kTileVec];
     tile_scan_ballots(sel, lane, warp, my_off, s_scan);
     __syncthreads();
-    if (warp == 0) {
+    if (warp == kTileWarps - 1) {
         const unsigned incl = tile_scan_finish(lane, s_scan);
         if (lane == 31) {
             s_misc[0] = incl;
-            s_misc[1] = (unsigned)(p.tags[t] & 0xffffffffull);  // this slot's previous same-parity count
+            s_misc[1] = prev_ld;
             if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);
             if (t == 0) *p.k_next = 0ull;
         }
@@ -182,6 +189,12 @@ __device__ __forceinline__ void encode_cta(const FusedStepParams& f, long long t
 }
 
 // ------------------------------------------------------------ decode CTA
+// A peer missed the timeout: GTC_EPEER on EVERY rank (system-scope atomics on
+// each rank's flags), so no replica carries on unaware; this CTA applies nothing.
+__device__ __forceinline__ void raise_peer_error(const FusedStepParams& f) {
+    if (threadIdx.x < (unsigned)f.nranks) atomicOr_system(f.peer_flags[threadIdx.x], kFlagPeer);
+}
+
 // Tiles [t0, t0 + ng) of every rank.  A peer timeout sets kFlagPeer.
 template <int MODE, typename Stamp>
 __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t0, int ng, signed char* s_cnt,
@@ -230,7 +243,7 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
         if ((unsigned)(tagv >> 32) != p.epoch) {
             const unsigned long long t0ns = now_ns();
             do {
-                if (now_ns() - t0ns > kTimeoutNs) {
+                if (now_ns() - t0ns > f.timeout_ns) {
                     *s_abort = 1;
                     break;
                 }
@@ -243,7 +256,7 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
     __syncthreads();
     stamp_ph(1);
     if (*s_abort) {
-        if (tid == 0) atomicOr(f.flags, kFlagPeer);
+        raise_peer_error(f);
         return;
     }
 
@@ -283,7 +296,7 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
 #pragma unroll
             for (int u = 0; u < kSpecPerThread; ++u)
                 if (((pend >> u) & 1u) && (e[u] >> kStampShift) == stamp) pend &= ~(1u << u);
-            if (pend && now_ns() - t_start > kTimeoutNs) ok = false;
+            if (pend && now_ns() - t_start > f.timeout_ns) ok = false;
         }
     };
     {
@@ -344,7 +357,7 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
     }
     stamp_ph(2);
     if (*s_abort) {
-        if (tid == 0) atomicOr(f.flags, kFlagPeer);
+        raise_peer_error(f);
         return;
     }
 
@@ -435,8 +448,9 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
     }
 }
 
+// CTA b of one rank's step.
 template <int CMP, bool HAS_G, int MODE>
-__global__ void __launch_bounds__(kTileThreads, 4) gtc_step_p2p_kernel(const FusedStepParams f) {
+__device__ __forceinline__ void step_cta(const FusedStepParams& f, long long b, long long trace_slot) {
     __shared__ unsigned s_scan[kTileVec * kTileWarps];
     __shared__ unsigned s_misc[2];
     __shared__ int4 s_cnt4[kDecGroup * kTile / 16];  // int8 counts of the decode CTA's tiles
@@ -445,15 +459,12 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_step_p2p_kernel(const Fus
     __shared__ __align__(128) unsigned long long s_rec[kPushRec / 8];  // the encode's push record
 
     const EncodeParams& p = f.enc;
-    const long long b = blockIdx.x;
-    const bool trace = f.trace && threadIdx.x == 0 && b < kStepTraceCtas;
+    const bool trace = f.trace && threadIdx.x == 0 && trace_slot < kStepTraceCtas;
     auto stamp_ph = [&](int ph) {
-        if (trace) g_step_trace[b * kStepTracePhases + ph] = now_ns();
+        if (trace) g_step_trace[trace_slot * kStepTracePhases + ph] = now_ns();
     };
-
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;");
     stamp_ph(0);
+    if (f.skip) return;  // loopback test hook: a rank that never shows up
 
     // CTA role: b < Q * (G + 1): group q = b / (G + 1), slot r = b % (G + 1);
     // r < G encodes tile q * G + r, r == G decodes group q - lag_groups; the
@@ -470,7 +481,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_step_p2p_kernel(const Fus
     if (trace) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_step_trace[b * kStepTracePhases + 5] = smid | (enc_tile < 0 ? 1u << 16 : 0u);
+        g_step_trace[trace_slot * kStepTracePhases + 5] = smid | (enc_tile < 0 ? 1u << 16 : 0u);
     }
     if (enc_tile >= 0) {
         if (enc_tile < p.num_tiles) encode_cta<CMP, HAS_G>(f, enc_tile, s_scan, s_misc, s_rec);
@@ -480,6 +491,30 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_step_p2p_kernel(const Fus
         decode_cta<MODE>(f, t0, ng, reinterpret_cast<signed char*>(s_cnt4), s_k, &s_abort, stamp_ph);
     }
     stamp_ph(4);
+}
+
+template <int CMP, bool HAS_G, int MODE>
+__global__ void __launch_bounds__(kTileThreads, 4) gtc_step_p2p_kernel(const FusedStepParams f) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    step_cta<CMP, HAS_G, MODE>(f, blockIdx.x, blockIdx.x);
+}
+
+// Loopback group (tests): the steps of `world` ranks of one process as ONE
+// launch.  Linear block b is CTA b / world of rank b % world, so every CTA a
+// decode CTA waits on (a lower CTA index of any rank) has a lower linear index
+// -- the same dispatch-order argument as the per-rank kernel.  Kernels that
+// wait on each other are never launched separately on one GPU.
+template <int CMP, bool HAS_G, int MODE>
+__global__ void __launch_bounds__(kTileThreads, 4)
+gtc_step_p2p_group_kernel(const FusedStepParams* __restrict__ group, int world) {
+    __shared__ FusedStepParams s_f;
+    const int rank = (int)(blockIdx.x % (unsigned)world);
+    const int* src = reinterpret_cast<const int*>(group + rank);
+    int* dst = reinterpret_cast<int*>(&s_f);
+    for (int i = threadIdx.x; i < (int)(sizeof(FusedStepParams) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    step_cta<CMP, HAS_G, MODE>(s_f, blockIdx.x / (unsigned)world, blockIdx.x);
 }
 
 template <int CMP, bool HAS_G, int MODE>
@@ -504,11 +539,27 @@ cudaError_t launch_g(FusedStepParams& f, int mode, cudaStream_t s) {
                                     : launch_t<CMP, HAS_G, GTC_ACCUM_WEIGHTS>(f, s);
 }
 
+template <int CMP, bool HAS_G, int MODE>
+cudaError_t launch_group_t(const FusedStepParams* group, const FusedStepParams& h, int world, cudaStream_t s) {
+    const long long Q = h.num_groups;
+    const long long per_rank = Q * (kDecGroup + 1) + std::min<long long>(h.lag_groups, Q);
+    gtc_step_p2p_group_kernel<CMP, HAS_G, MODE><<<(unsigned)(per_rank * world), kTileThreads, 0, s>>>(group, world);
+    return cudaGetLastError();
+}
+
+template <int CMP, bool HAS_G>
+cudaError_t launch_group_g(const FusedStepParams* group, const FusedStepParams& h, int world, int mode,
+                           cudaStream_t s) {
+    if (mode == GTC_ACCUM_MOMENTUM) return launch_group_t<CMP, HAS_G, GTC_ACCUM_MOMENTUM>(group, h, world, s);
+    return mode == GTC_ACCUM_UPDATE ? launch_group_t<CMP, HAS_G, GTC_ACCUM_UPDATE>(group, h, world, s)
+                                    : launch_group_t<CMP, HAS_G, GTC_ACCUM_WEIGHTS>(group, h, world, s);
+}
+
 }  // namespace
 
-// Decode lag in groups: about one wave of resident CTAs (GTC_FUSED_LAG, in
-// tiles, overrides).
-int step_p2p_lag_groups(int num_tiles) {
+// Decode lag in groups: about one wave of resident CTAs of one rank
+// (GTC_FUSED_LAG, in tiles, overrides).
+int step_p2p_lag_groups(int num_tiles, int ranks_per_device) {
     static std::once_flag once;
     static int wave = 592;
     std::call_once(once, [] {
@@ -519,11 +570,13 @@ int step_p2p_lag_groups(int num_tiles) {
                 &per_sm, gtc_step_p2p_kernel<GTC_CMP_GT, true, GTC_ACCUM_WEIGHTS>, kTileThreads, 0) == cudaSuccess &&
             sms > 0 && per_sm > 0)
             wave = sms * per_sm;
-        const char* e = std::getenv("GTC_FUSED_LAG");
-        if (e && std::atoi(e) > 0) wave = std::atoi(e);
     });
+    int w = wave / std::max(1, ranks_per_device);
+    if (const char* e = std::getenv("GTC_FUSED_LAG")) {  // read per step: tests vary it
+        if (std::atoi(e) > 0) w = std::atoi(e);
+    }
     const int groups = (num_tiles + kDecGroup - 1) / kDecGroup;
-    const int lag = (wave + kDecGroup) / (kDecGroup + 1);  // groups of G + 1 CTAs per wave
+    const int lag = (w + kDecGroup) / (kDecGroup + 1);  // groups of G + 1 CTAs per wave
     return std::max(1, std::min(lag, groups));
 }
 
@@ -539,6 +592,19 @@ cudaError_t launch_step_p2p(FusedStepParams& f, int cmp_mode, int accum_mode, cu
     if (cmp_mode == GTC_CMP_GE)
         return f.enc.g ? launch_g<GTC_CMP_GE, true>(f, accum_mode, s) : launch_g<GTC_CMP_GE, false>(f, accum_mode, s);
     return f.enc.g ? launch_g<GTC_CMP_GT, true>(f, accum_mode, s) : launch_g<GTC_CMP_GT, false>(f, accum_mode, s);
+}
+
+// `host` is rank 0's parameters (num_groups, lag_groups set by the caller,
+// identical on every rank); HAS_G from rank 0 (all ranks pass grad or none).
+cudaError_t launch_step_p2p_group(const FusedStepParams* group, const FusedStepParams& h, int world, int cmp_mode,
+                                  int accum_mode, cudaStream_t s) {
+    if (h.enc.num_tiles == 0) return cudaSuccess;
+    const bool g = h.enc.g != nullptr;
+    if (cmp_mode == GTC_CMP_GE)
+        return g ? launch_group_g<GTC_CMP_GE, true>(group, h, world, accum_mode, s)
+                 : launch_group_g<GTC_CMP_GE, false>(group, h, world, accum_mode, s);
+    return g ? launch_group_g<GTC_CMP_GT, true>(group, h, world, accum_mode, s)
+             : launch_group_g<GTC_CMP_GT, false>(group, h, world, accum_mode, s);
 }
 
 }  // namespace gtc

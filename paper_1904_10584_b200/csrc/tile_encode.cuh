@@ -58,6 +58,14 @@ __device__ __forceinline__ void st_stream(float4* p, const float4& v) {
                  :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
+// The count half of a tile tag (tags are little-endian u64: count in the low
+// word); asm volatile so it is issued where it is written, before the tile loads.
+__device__ __forceinline__ unsigned ld_tag_count(const unsigned long long* tag) {
+    unsigned v;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(tag));
+    return v;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -5,8 +5,9 @@ It holds none of the method's arithmetic -- no thresholding, no residual update,
 no packing -- only the input recipe of DESIGN.md Sec. "Inputs": gradient vectors
 shaped like the paper's LSTM acoustic model (Sec. II-B:
 5 LSTM layers x 768 units on 64x3 stacked log-mel input, 3,183 senones) with
-seeded numpy Philox streams.  Every value is float32 and produced on the host;
-callers copy it to the GPU themselves.
+seeded numpy Philox streams.  Every value is float32 and produced on the host
+(callers copy it to the GPU themselves), except ``cuda_normal``, which draws
+the 1e9-parameter gradients on the GPU with torch's seeded Philox generator.
 """
 from __future__ import annotations
 
@@ -132,3 +133,40 @@ def sigma_for_density(rho: float, tau: float, mean_scale: float = 1.0) -> float:
     g ~ s*N(0, sigma), P(|r0+g| crosses tau) ~= E|g| / (2 tau)
     = sigma * mean_scale * sqrt(2/pi) / (2 tau).  Solve for sigma."""
     return rho * tau * math.sqrt(2.0 * math.pi) / mean_scale
+
+
+def cuda_normal(n: int, seed: int, step: int, rank: int = 0, device="cuda"):
+    """i.i.d. N(0,1) float32 of length n generated ON THE GPU (torch's Philox
+    generator seeded with (rank_seed(rank, seed) + step) mod 2^63).  For the
+    1e9-parameter config (BASELINE configs[4]) where a host generator would
+    take longer than the run; the oracle side copies back the windows it
+    checks.  Holds no arithmetic of the method."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    gen.manual_seed((rank_seed(rank, seed) + 1_000_003 * step) % (1 << 63))
+    return torch.randn(n, generator=gen, dtype=torch.float32, device=device)
+
+
+def sigma_for_cycle_density(rho: float, tau: float, mean_scale: float = 1.0, n_buffers: int = 1,
+                            correlated: float = 0.0) -> float:
+    """Input calibration of the benchmark (not part of the method).  The bench
+    applies n_buffers fixed gradients in rotation, so every element drifts by
+    d = sum_j g_j per cycle and, once the residual is stationary, sends |d|/tau
+    quanta per cycle: rho = E|d| / (n_buffers * tau) = sigma_e * sqrt(2/pi) /
+    (sqrt(n_buffers) * tau), with sigma_e = sigma * mean_scale * sqrt(1 + c^2)
+    for lstm_gradient(..., correlated=c).  Solve for sigma."""
+    return rho * tau * math.sqrt(n_buffers) / (mean_scale * math.sqrt(2.0 / math.pi) *
+                                               math.sqrt(1.0 + correlated * correlated))
+
+
+def steady_residual(grads, tau: float, seed: int) -> np.ndarray:
+    """A stationary residual for gradients applied in rotation:
+    r0 = sign(sum_j g_j) * U(0, tau) (an element drifting up sits in (0, tau]
+    between quanta), so the measured density equals sigma_for_cycle_density's
+    target from the first step instead of after ~500 steps."""
+    d = np.zeros(grads[0].size, dtype=np.float64)
+    for g in grads:
+        d += g
+    u = uniform(grads[0].size, 0.0, tau, seed)
+    return np.where(d < 0, -u, u).astype(np.float32)

@@ -78,8 +78,7 @@ def main():
         hs = [None] * world
         dist.all_gather_object(hs, h)
         assert len(set(hs)) == 1, f"replicas differ at step {t}"
-    # the one-call step (p2p: one fused encode+exchange+decode kernel, or the
-    # pipelined chunks with GTC_PIPELINE_CHUNKS > 1); odd steps start the ranks
+    # the one-call step (p2p: one fused encode+exchange+decode kernel); odd steps start the ranks
     # at different times so the in-kernel waits on peers' tiles are exercised
     for t in range(steps, 2 * steps):
         gs = [synth.correlated_gradient(n, 4.0, synth.BASE_SEED, t, w) for w in range(world)]

@@ -1,0 +1,179 @@
+"""Config 5 (BASELINE.json configs[4]): 1e9 parameters, 100 steps from r = 0 --
+the residual-stability run of PAPER.md:222 ("The residual gradients which are
+not sent ... are aggregated locally for later iterations").
+
+g_t ~ N(0,1) i.i.d. per rank and step (drawn on the GPU, synth.cuda_normal),
+tau = 8, GT mode, ACCUM_WEIGHTS.  Every step reports density k/n, max|r| and
+the conservation error on a 1e6-element float64 shadow [0, 1e6):
+
+    | r_T + tau * sum_t s_t  -  sum_t g_t |  <=  sum_t ulp(v_t) / 2
+
+(the only rounding is v = fl(r + g); r - s*tau is exact for tau = 8 = 2^3,
+SURVEY O14), with s_t read from the MESSAGES, not from the residual.  The
+shadow also checks |r_new| <= max(tau, |v| - tau) element by element.  At
+steps 1, 10, 20, ..., 100 one oracle step runs from the GPU's r_{t-1} on 14
+sampled windows (incl. the ragged last tile) and the window's messages,
+counts, r_t and weights must match bit-exactly.
+
+world 1 runs the one-kernel gtc_step; world 4 runs a loopback group on one GPU
+(the separate p2p calls, ~85 GB of HBM).  GTC_C5_REPORT=<path> writes the
+per-step series as JSON.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1904_10584_b200 as gtc  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+N = 1_000_000_000
+TAU = 8.0
+STEPS = 100
+SHADOW = 1_000_000
+ALPHA = -1e-4
+CHECK_STEPS = {1} | set(range(10, STEPS + 1, 10))
+
+
+def windows(n):
+    rng = np.random.default_rng(1904)
+    starts = sorted(int(x) for x in rng.integers(SHADOW, n - 70_000, size=12))
+    return [(0, 65_536)] + [(a, a + 65_536) for a in starts] + [(n - 70_000, n)]  # last: ragged tile
+
+
+def window_words(msg_i64, a, b):
+    """Words of [a, b) of a canonical message (int64 view of the uint32
+    words), re-indexed to the window: ((i - a) << 1) | neg."""
+    idx = msg_i64 >> 1
+    lo = int(torch.searchsorted(idx, a))
+    hi = int(torch.searchsorted(idx, b))
+    w = msg_i64[lo:hi].cpu().numpy()
+    return ((((w >> 1) - a) << 1) | (w & 1)).astype(np.uint32)
+
+
+def as_u64(t):
+    return t.to(torch.int64) & 0xFFFFFFFF
+
+
+def run_c5(world):
+    Wn = windows(N)
+    report = {"n": N, "world": world, "tau": TAU, "steps": STEPS, "density": [], "max_abs_r": [],
+              "conservation_max_err": [], "conservation_max_bound": [], "oracle_checked_steps": []}
+    if world == 1:
+        grp = None
+        ranks = [gtc.GTC(N, TAU, max_words_per_rank=N // 20)]
+    else:
+        grp = gtc.LoopbackGroup(N, TAU, world, DEV, max_words_per_rank=N // 20)
+        ranks = grp.ranks
+    r = [torch.zeros(N, dtype=torch.float32, device=DEV) for _ in range(world)]
+    w0 = synth.cuda_normal(N, synth.BASE_SEED, 10_000) * 0.05
+    w = [w0] + [w0.clone() for _ in range(world - 1)]
+    cnt = torch.empty(N, dtype=torch.int8, device=DEV) if world > 1 else None
+    # float64 shadow of rank 0 on [0, SHADOW)
+    g_sum = np.zeros(SHADOW, np.float64)
+    q_sum = np.zeros(SHADOW, np.int64)
+    bound = np.zeros(SHADOW, np.float64)
+    r_prev = np.zeros(SHADOW, np.float32)
+    g = None
+    for t in range(1, STEPS + 1):
+        check = t in CHECK_STEPS
+        if check:
+            rw = [[r[m][a:b].cpu().numpy() for (a, b) in Wn] for m in range(world)]
+            ww = [w[0][a:b].cpu().numpy() for (a, b) in Wn]
+            gw = [[None] * len(Wn) for _ in range(world)]
+        if world == 1:
+            g = synth.cuda_normal(N, synth.BASE_SEED, t, 0)
+            g0 = g[:SHADOW].cpu().numpy()
+            if check:
+                gw[0] = [g[a:b].cpu().numpy() for (a, b) in Wn]
+            assert ranks[0].step(g, r[0], w[0], ALPHA) == gtc.GTC_OK
+        else:
+            # the separate p2p calls of a loopback group: every encode (one
+            # gradient buffer, regenerated per rank), every exchange, every decode
+            for m in range(world):
+                g = synth.cuda_normal(N, synth.BASE_SEED, t, m)
+                if m == 0:
+                    g0 = g[:SHADOW].cpu().numpy()
+                if check:
+                    gw[m] = [g[a:b].cpu().numpy() for (a, b) in Wn]
+                ranks[m].encode(g, r[m])
+            for m in range(world):
+                assert ranks[m].exchange() == gtc.GTC_OK
+            for m in range(world):
+                ranks[m].decode_apply(w[m], ALPHA, gtc.GTC_ACCUM_WEIGHTS, cnt if (check and m == 0) else None)
+        torch.cuda.synchronize()
+        k = ranks[0].last_counts()
+        report["density"].append([kk / N for kk in k])
+        report["max_abs_r"].append(max(max(-float(lo), float(hi)) for lo, hi in (x.aminmax() for x in r)))
+        # shadow: quanta from rank 0's message (ascending words: a prefix)
+        _, k0 = ranks[0].message(0)
+        msg0 = as_u64(ranks[0].message_tensor(0))
+        assert msg0.numel() == k[0] == k0
+        head = window_words(msg0, 0, SHADOW)
+        q_sum[head >> 1] += 1 - 2 * (head & 1).astype(np.int64)
+        v = (r_prev + g0).astype(np.float32)  # fl(r + g), the step's only rounding
+        g_sum += g0.astype(np.float64)
+        bound += np.abs(v.astype(np.float64)) * 2.0 ** -24
+        r_now = r[0][:SHADOW].cpu().numpy()
+        assert np.all(np.abs(r_now) <= np.maximum(TAU, np.abs(v) - TAU)), f"step {t}: |r| bound"
+        err = np.abs(r_now.astype(np.float64) + TAU * q_sum - g_sum)
+        assert np.all(err <= bound + 1e-10), f"step {t}: conservation {err.max()} > bound"
+        report["conservation_max_err"].append(float(err.max()))
+        report["conservation_max_bound"].append(float(bound.max()))
+        r_prev = r_now
+        if world > 1:
+            for m in range(1, world):
+                assert torch.equal(w[0], w[m]), f"step {t}: replica {m} differs"
+        if check:
+            msgs = [as_u64(ranks[0].message_tensor(m)) for m in range(world)]
+            for j, (a, b) in enumerate(Wn):
+                rs = [rw[m][j].copy() for m in range(world)]
+                wo = ww[j].copy()
+                om, oc, _ = oracle.step([gw[m][j] for m in range(world)], rs, wo, TAU, oracle.CMP_GT, ALPHA,
+                                        oracle.ACCUM_WEIGHTS)
+                for m in range(world):
+                    assert np.array_equal(window_words(msgs[m], a, b), om[m]), f"step {t} window {a}: msg {m}"
+                    got_r = r[m][a:b].cpu().numpy()
+                    assert np.array_equal(got_r.view(np.uint32), rs[m].view(np.uint32)), f"step {t} window {a}: r"
+                if cnt is not None:
+                    assert np.array_equal(cnt[a:b].cpu().numpy().astype(np.int32), oc), f"step {t} window {a}: c"
+                assert np.array_equal(w[0][a:b].cpu().numpy().view(np.uint32), wo.view(np.uint32)), \
+                    f"step {t} window {a}: weights"
+            report["oracle_checked_steps"].append(t)
+        for st in (grp.check() if grp else [ranks[0].check()]):
+            assert st == gtc.GTC_OK
+    dens = [d[0] for d in report["density"]]
+    # SURVEY appendix (tau = 8, N(0,1) from r = 0): ~0 at step 1, 1.36 % at step 100
+    assert dens[0] < 1e-8
+    assert 0.009 < dens[-1] < 0.019, dens[-1]
+    assert dens[0] < dens[9] < dens[49] < dens[99]  # climbing while r fills up
+    path = os.environ.get("GTC_C5_REPORT")
+    if path:
+        with open(path if world == 1 else path.replace(".json", f"_world{world}.json"), "w") as f:
+            json.dump(report, f)
+    print(f"C5 world={world}: density {dens[0]:.2e} -> {dens[-1]:.4%}, max|r| {max(report['max_abs_r']):.3f}, "
+          f"conservation max err {max(report['conservation_max_err']):.3e} "
+          f"(bound {max(report['conservation_max_bound']):.3e}), oracle steps {report['oracle_checked_steps']}")
+    if grp:
+        grp.close()
+    else:
+        ranks[0].close()
+
+
+def test_config5_1e9_100_steps_world1():
+    run_c5(1)
+
+
+@pytest.mark.skipif(torch.cuda.get_device_properties(0).total_memory < 120 * 2**30, reason="needs ~90 GB")
+def test_config5_1e9_100_steps_loopback_world4():
+    run_c5(4)

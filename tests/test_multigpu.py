@@ -45,11 +45,11 @@ def test_exchange_lstm_am_size(exchange):
 def test_momentum_multigpu(world, exchange):
     """GTC_ACCUM_MOMENTUM (SGD-momentum apply, reading M1): weights, momentum
     buffer, residuals, messages and counts bit-exact with the oracle; also the
-    pipelined one-call step."""
+    one-call step."""
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="3", GTC_N="1000003", GTC_EXCHANGE=exchange,
-               GTC_ACCUM="momentum", GTC_PIPELINE_CHUNKS="2")
+               GTC_ACCUM="momentum")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29535", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
@@ -70,18 +70,6 @@ def test_bmuf_multigpu(world, exchange):
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "BMUF OK" in p.stdout
-
-
-def test_pipelined_step_parity():
-    """gtc_step with the p2p pipeline switched on (GTC_PIPELINE_CHUNKS=3)."""
-    if ngpus() < 2:
-        pytest.skip("needs 2 GPUs")
-    env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="4", GTC_N="1000003", GTC_EXCHANGE="p2p",
-               GTC_PIPELINE_CHUNKS="3")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
-    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
 
 @pytest.mark.parametrize("world,lag,accum", [(2, "1", "weights"), (2, "7", "update"), (3, "64", "weights"),
