@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--split-step", action="store_true",
                     help="world > 1, p2p: gtc_step as encode + decode_apply kernels (GTC_STEP_SPLIT) "
                          "instead of the one fused kernel")
+    ap.add_argument("--sharded", action="store_true",
+                    help="world > 1, p2p: owner-computes decode (GTC_DECODE_SHARDED, SURVEY 8(f) #4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -153,13 +155,35 @@ def n_grad_buffers(n):
 
 
 def make_inputs(n, tau, rho, rank, world):
-    """Per-rank synthetic inputs (host): LSTM-shaped gradients, r0 ~ U(-tau, tau), w0."""
-    sigma = synth.sigma_for_density(rho, tau, synth.mean_abs_scale(n))
+    """Per-rank synthetic inputs (host): LSTM-shaped gradients applied in
+    rotation, calibrated so the STATIONARY density is rho
+    (synth.sigma_for_cycle_density), a stationary residual
+    (synth.steady_residual: the density holds from the first step) and the
+    replicated weights w0."""
+    nb = n_grad_buffers(n)
     corr = 0.5 if world > 1 else 0.0
-    grads = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, rank, corr) for t in range(n_grad_buffers(n))]
-    r0 = synth.uniform(n, -tau, tau, synth.rank_seed(rank))
+    sigma = synth.sigma_for_cycle_density(rho, tau, synth.mean_abs_scale(n), nb, corr)
+    grads = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, rank, corr) for t in range(nb)]
+    r0 = synth.steady_residual(grads, tau, synth.rank_seed(rank))
     w0 = synth.normal(n, synth.BASE_SEED, 0, 11) * np.float32(0.05)  # replicated weights
     return grads, r0, w0
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except AttributeError:
+        affinity = os.cpu_count()
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity": affinity}
 
 
 # ------------------------------------------------------------------ oracle legs
@@ -194,9 +218,9 @@ def cpu_oracle_run(n_full, tau, rho, cmp, alpha, budget_s, world=1, inputs=None,
         if steps >= 200:
             break
     value = world * n * steps / t_used
-    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{steps} full steps of the {n}-param workload x {world} simulated worker(s) "
-                      f"(oracle.step: encode+aggregate+apply, single thread), {t_used:.1f} s"}
+    return dict({"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                 "sample": f"{steps} full steps of the {n}-param workload x {world} simulated worker(s) "
+                           f"(oracle.step: encode+aggregate+apply, single thread), {t_used:.1f} s"}, **cpu_info())
 
 
 def run_reference(args):
@@ -231,11 +255,53 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": args.workload, "n_params": n_full, "sample_params": n,
                                         "tau": args.tau, "rho_target": args.rho, "cmp": args.cmp,
                                         "apply": "ACCUM_MOMENTUM" if args.accum == "momentum" else "ACCUM_WEIGHTS"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+                             **cpu_info()),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+class NvlinkCounters:
+    """NVLink data counters of one GPU (NVML field values, KiB), sampled
+    around the timed region; None where the driver does not expose them."""
+
+    TX, RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+
+    def __init__(self, gpu_index):
+        self.h = None
+        self.err = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        except Exception as e:  # no NVML: report why
+            self.err = f"nvml: {e}"
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, [self.TX, self.RX])
+            out = []
+            for v in vals:
+                if v.nvmlReturn != 0:
+                    self.err = f"field {v.fieldId}: nvml return {v.nvmlReturn}"
+                    return None
+                out.append(int(v.value.ullVal))
+            return out
+        except Exception as e:
+            self.err = f"nvml read: {e}"
+            return None
+
+    @staticmethod
+    def delta(a, b):
+        if a is None or b is None:
+            return None
+        return {"tx_bytes": 1024 * (b[0] - a[0]), "rx_bytes": 1024 * (b[1] - a[1])}
 
 
 # ------------------------------------------------------------------ GPU leg
@@ -264,13 +330,19 @@ def run_gtc(args):
     # at 1e9 params cap it at 5 % of n to save 3 GB per rank
     cap = 0 if n < 100_000_000 or args.exchange == "nccl" else n // 20
     ctx = gtc.GTC(n, tau, rank, world, dev, cmp=args.cmp, exchange=args.exchange, max_words_per_rank=cap,
-                  fused_step=not args.split_step)
+                  fused_step=not args.split_step, sharded=args.sharded and world > 1)
     stream = torch.cuda.current_stream(dev)
     momentum = args.accum == "momentum"
     amode = gtc.GTC_ACCUM_MOMENTUM if momentum else gtc.GTC_ACCUM_WEIGHTS
     if momentum:
         mbuf = torch.zeros(n, dtype=torch.float32, device=dev)
         ctx.bind_momentum(mbuf, args.mu)
+
+    def allmax(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
     def step(t):
         ctx.encode(grads[t % NB], r)
@@ -287,61 +359,71 @@ def run_gtc(args):
     stepf(0)
     torch.cuda.synchronize()
     one_kernel = ctx.kernel_launches() - l0 == 1
+    assert ctx.check() == gtc.GTC_OK
 
     # Timed region: K steps through the one-call C entry point (gtc_step: one
-    # fused kernel at world 1 and, p2p, at world > 1).  Every EV_EVERY-th step
-    # is bracketed by CUDA events (same stream): with one kernel per step that
-    # is the kernel's duration; otherwise (NCCL exchange, momentum at world > 1)
-    # those steps run as the three separate calls with events between them
-    # (per-kernel durations).
+    # fused kernel at world 1 and, p2p, at world > 1).  With more than one
+    # kernel per step (NCCL exchange, --split-step, momentum at world > 1)
+    # every EV_EVERY-th step runs as the three separate calls with CUDA events
+    # between them (per-phase durations).
     K = args.steps
     EV_EVERY = 8
-    inst = [t for t in range(K) if t % EV_EVERY == 0]
+    inst = [] if one_kernel else [t for t in range(K) if t % EV_EVERY == 0]
     ev = {t: [torch.cuda.Event(enable_timing=True) for _ in range(4)] for t in inst}
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local_rank)
     clocks.start()
+    nvl = NvlinkCounters(local_rank)
     time.sleep(0.6)
     launches0 = ctx.kernel_launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark()
+    nvl0 = nvl.read()
     e_start.record(stream)
     for t in range(K):
-        if t % EV_EVERY == 0:
+        if t in ev:
             e = ev[t]
-            if one_kernel:
-                e[0].record(stream)
-                stepf(t)
-                e[1].record(stream)
-                e[2].record(stream)
-                e[3].record(stream)
-            else:
-                e[0].record(stream)
-                ctx.encode(grads[t % NB], r)
-                e[1].record(stream)
-                ctx.exchange()
-                e[2].record(stream)
-                ctx.decode_apply(w, args.alpha, amode)
-                e[3].record(stream)
+            e[0].record(stream)
+            ctx.encode(grads[t % NB], r)
+            e[1].record(stream)
+            ctx.exchange()
+            e[2].record(stream)
+            ctx.decode_apply(w, args.alpha, amode)
+            e[3].record(stream)
         else:
             stepf(t)
     e_end.record(stream)
     torch.cuda.synchronize()
+    nvl1 = nvl.read()
     if world > 1:
         dist.barrier()
     clocks.mark()
     launches = ctx.kernel_launches() - launches0
     time.sleep(0.3)
     clocks.stop()
+    # device-side faults (GTC_EPEER, GTC_ENONFINITE) are sticky: a faulted
+    # run is not a measurement
+    status = int(allmax([float(ctx.check())])[0])
+    if status != gtc.GTC_OK:
+        raise SystemExit(f"bench: timed steps faulted on some rank: {gtc.gtc_strerror(status)}")
 
     ms_local = e_start.elapsed_time(e_end)
-    enc_ms = sum(ev[t][0].elapsed_time(ev[t][1]) for t in inst) / len(inst)
-    exch_ms = sum(ev[t][1].elapsed_time(ev[t][2]) for t in inst) / len(inst)
-    dec_ms = sum(ev[t][2].elapsed_time(ev[t][3]) for t in inst) / len(inst)
-    ks_local = ctx.last_counts()
-    k_rank = ks_local[rank] if world > 1 else ks_local[0]
+    phases = None
+    if inst:
+        phases = [sum(ev[t][i].elapsed_time(ev[t][i + 1]) for t in inst) / len(inst) for i in range(3)]
+
+    # density over the timed steps' regime (untimed: the inputs are
+    # stationary, so the next M steps sample the same distribution)
+    M = min(K, 64)
+    ks = []
+    for t in range(K, K + M):
+        stepf(t)
+        ks.append(ctx.last_counts())  # waits
+    k_rank = [kk[rank if world > 1 else 0] for kk in ks]
+    k_mean = float(np.mean(k_rank))
+    k_all_mean = [float(np.mean([kk[m] for kk in ks])) for m in range(world)]
 
     # unfused breakdown (untimed by the step metric): the encode kernel alone
     # and the exchange + decode alone (separate calls), CUDA events on the stream
@@ -359,34 +441,53 @@ def run_gtc(args):
             ctx.decode_apply(w, args.alpha, amode)
             eb[t][2].record(stream)
         torch.cuda.synchronize()
-        bt = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in eb) / B,
-                           sum(e[1].elapsed_time(e[2]) for e in eb) / B], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(bt, op=dist.ReduceOp.MAX)
-        brk = {"encode_only_ms": bt[0].item(), "decode_only_ms": bt[1].item()}
+        bt = allmax([sum(e[0].elapsed_time(e[1]) for e in eb) / B, sum(e[1].elapsed_time(e[2]) for e in eb) / B])
+        brk = {"encode_only_ms": bt[0], "decode_only_ms": bt[1]}
 
-    # density of the touched set (for the decode's algorithmic bytes), untimed
+    # touched set of one step (decode's algorithmic bytes; the sector floor)
     cnt = torch.empty(n, dtype=torch.int8, device=dev)
     ctx.encode(grads[K % NB], r)
     ctx.exchange()
     ctx.decode_apply(w, args.alpha, amode, cnt)
-    nnz_c = int(torch.count_nonzero(cnt).item())
-    k_all = ctx.last_counts()
-    del cnt
+    nz = torch.nonzero(cnt).flatten()
+    nnz_c = int(nz.numel())
+    sectors_c = int(torch.unique_consecutive(nz // 8).numel())  # distinct 32-byte sectors of the target
+    del cnt, nz
 
-    stats = torch.tensor([ms_local, enc_ms, exch_ms, dec_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    ms, enc_ms_max, exch_ms_max, dec_ms_max = stats.tolist()
+    # residual-aliased gradient: the caller's backward
+    # accumulates into r, then gtc_step(grad = NULL) encodes at 8 B/param
+    # instead of 12.  Stand-in backward: torch's r.add_(g).  The step's time
+    # is (add_ + gtc_step(NULL) loop) - (add_ loop), each loop timed whole
+    # (per-step events would stall the stream and hide nothing less).
+    GN = 64
+    sp = stream.cuda_stream
+    lib = gtc.load_library()
+    rp, wp = r.data_ptr(), w.data_ptr()
+
+    def loop(with_step):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for t in range(GN):
+            r.add_(grads[t % NB])
+            if with_step:
+                lib.gtc_step(ctx.ctx, None, rp, wp, args.alpha, amode, sp)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / GN
+
+    loop(True)  # warm
+    add_ms = allmax([loop(False)])[0]
+    both_ms = allmax([loop(True)])[0]
+    gn_ms = both_ms - add_ms
+    assert ctx.check() == gtc.GTC_OK
+
+    ms, = allmax([ms_local])
     ms_per_step = ms / K
-    enc_ms_events = enc_ms
-    if one_kernel:
-        # the step IS one kernel (world 1: the fused encode + apply; world > 1:
-        # the fused encode + exchange + decode + apply); its average
-        # launch duration over the timed region, launch gaps included, is the
-        # region's event time / K (the bracketing events of the sampled steps
-        # stall the stream and would overstate it)
-        enc_ms = ms_per_step
+    if phases is not None:
+        phases = allmax(phases)
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -413,107 +514,123 @@ def run_gtc(args):
             _ = int(k_host[0])
         s1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = torch.tensor([s0.elapsed_time(s1) / E], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n / (e2e_ms.item() * 1e-3), "unit": UNIT,
+        e2e_ms = allmax([s0.elapsed_time(s1) / E])[0]
+        e2e = {"value": world * n / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,
-               "ms_per_step": e2e_ms.item(),
-               "note": "pinned host gradient -> device copy + encode/exchange/decode_apply + k read back, per step"}
+               "ms_per_step": e2e_ms,
+               "note": "pinned host gradient -> device copy + gtc_step + k read back, per step"}
         del gdev
+        assert ctx.check() == gtc.GTC_OK
 
     if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        ctx.close()
+        ctx.close()  # collective at world > 1 (quiesce)
+        dist.barrier()
+        dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel and the decode
+    # ---- roofline of the dominant kernel
     peak, peak_src = measured_peaks()
-    ntiles = math.ceil(n / gtc.GTC_TILE)
-    nvl_bytes = 0
+    T = math.ceil(n / gtc.GTC_TILE)
+    k = k_mean
+    K_all = sum(k_all_mean)
+    nvl_bytes = 0.0
+    rmw = 16 * n if momentum else 8 * (k if world == 1 else nnz_c)
+    rmw_floor = 16 * n if momentum else 64 * sectors_c  # 32-byte sectors read + written
     if world == 1:
         # the fused step kernel: stream g, r -> r (12 B/param), words (4 k),
         # tags (8 B/tile), target read-modify-write of the k touched elements
-        enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles + (16 * n if momentum else 8 * k_rank)
+        base = 12 * n + 4 * k + 8 * T
         kernel_name = "gtc_encode_tile_kernel (fused apply, world 1)"
     elif one_kernel:
         # the fused p2p step kernel, local HBM: the encode (12 n + 4 k + 8 T),
         # this rank's words and tags read back by the decode (4 k + 8 T), the
-        # target read-modify-write of the touched elements (8 nnz; momentum:
-        # w and buf read and written, 16 n); the peers'
-        # words and tags cross NVLink (nvlink_bytes_per_rank)
-        enc_bytes = 12 * n + 8 * k_rank + 16 * ntiles + (16 * n if momentum else 8 * nnz_c)
-        nvl_bytes = 4 * (sum(k_all) - k_rank) + 16 * (world - 1) * ntiles  # records: 16-byte header + entries
+        # pushed records landing here ((N-1) records), the target RMW
+        base = 12 * n + 8 * k + 16 * T
+        nvl_bytes = 4 * (K_all - k) + 16 * (world - 1) * T  # records: 16-byte header + entries
         kernel_name = "gtc_step_p2p_kernel (fused encode + exchange + decode + apply)"
     else:
-        enc_bytes = 12 * n + 4 * k_rank + 8 * ntiles
+        base = 12 * n + 4 * k + 8 * T
+        rmw = rmw_floor = 0
         kernel_name = "gtc_encode_tile_kernel"
-    enc_gbs = enc_bytes / (enc_ms * 1e-3) / 1e9
-    sum_k = sum(k_all)
-    # decode: words + tags read, then the apply (sparse: 8 B per non-zero
-    # count; momentum: w and buf read and written, 16 B per parameter)
-    dec_bytes = 4 * sum_k + 8 * world * ntiles + (16 * n if momentum else 8 * nnz_c)
-    dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9 if world > 1 and dec_ms > 0 else None
-    step_bytes = enc_bytes + (dec_bytes + 4 * (world - 1) * max(k_all) if world > 1 and not one_kernel else 0)
-    # DRAM traffic per launch from the committed ncu capture of the encode
-    # kernel; none for the world > 1 one-kernel step (ncu cannot replay it:
-    # its CTAs wait on the peers' pushes)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "encode_dram_bytes.json")
-    if os.path.exists(tpath) and not (world > 1 and one_kernel) and not momentum:
+    alg_bytes = base + rmw
+    floor_bytes = base + rmw_floor
+    kern_ms = ms_per_step if one_kernel else phases[0]
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    # DRAM traffic per launch from the committed warm, back-to-back ncu capture
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            if tj.get("workload") == args.workload and tj.get("n") == n:
-                traffic = tj.get("dram_bytes_per_launch")
+            key = f"{args.workload}/n{world}/{args.accum}/{'fused' if one_kernel else 'split'}"
+            if key in tj and tj[key].get("rho_target") == args.rho:
+                traffic, traffic_src = tj[key]["dram_bytes_per_launch"], tj[key]["source"]
         except Exception:
             traffic = None
-
+    roofline = {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "alg_bytes_per_launch": alg_bytes, "ms_per_launch": kern_ms, "peak_source": peak_src,
+                "sector_floor_bytes_per_launch": floor_bytes,
+                "frac_sector_floor": floor_bytes / (kern_ms * 1e-3) / 1e9 / peak,
+                "touched_elements": nnz_c, "touched_sectors": sectors_c,
+                "share_of_step": kern_ms / ms_per_step}
+    if world > 1:
+        nv_delta = NvlinkCounters.delta(nvl0, nvl1)
+        roofline["nvlink"] = {
+            "bytes_per_step_per_rank": nvl_bytes if one_kernel else 4 * (world - 1) * max(k_all_mean),
+            "frac_of_900GBs": (nvl_bytes if one_kernel else 4 * (world - 1) * max(k_all_mean))
+            / (ms_per_step * 1e-3) / 900e9,
+            "frac_of_770GBs_measured_peer_copy": (nvl_bytes if one_kernel else 4 * (world - 1) * max(k_all_mean))
+            / (ms_per_step * 1e-3) / 770e9,
+            "counters_timed_region": None if nv_delta is None else
+            {kk: v / K for kk, v in nv_delta.items()},  # per step
+            "counters_note": "NVML NVLink data counters of rank 0's GPU over the timed region, per step"
+            if nv_delta is not None else (nvl.err or "unavailable")}
+    gn_bytes = base - 4 * n + rmw  # grad = NULL: no 4 n gradient read
+    line = {
+        "metric": METRIC, "value": world * n / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": wl["desc"], "n_params": n, "tau": tau,
+                   "rho_target": args.rho, "rho_measured_mean": k / n,
+                   "rho_measured_min": min(k_rank) / n, "rho_measured_max": max(k_rank) / n,
+                   "rho_note": f"k per step of rank {rank} over {M} steps after the timed region (same stationary "
+                               "inputs: steady-state residual, gradients in rotation)",
+                   "cmp": args.cmp, "parallelism": f"dp{world}",
+                   "apply": f"ACCUM_MOMENTUM (mu={args.mu})" if momentum else "ACCUM_WEIGHTS",
+                   "exchange": ctx.exchange_mode() + (" sharded (owner-computes)" if args.sharded and world > 1
+                                                      else ""),
+                   "step": "one kernel" if one_kernel else "separate kernels",
+                   "l2": f"inputs larger than L2: g rotates over {NB} buffer(s), "
+                         f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},
+        "roofline": roofline,
+        "kernels": {"phases_ms": None if phases is None else
+                    {"encode": phases[0], "exchange": phases[1], "decode_apply": phases[2]},
+                    "unfused_breakdown": brk, "k_per_rank_mean": k_all_mean, "nnz_counts": nnz_c},
+        "grad_null": {"ms_per_step": gn_ms, "alg_bytes_per_launch": gn_bytes,
+                      "achieved_GBs": gn_bytes / (gn_ms * 1e-3) / 1e9,
+                      "frac": gn_bytes / (gn_ms * 1e-3) / 1e9 / peak,
+                      "params_per_s": world * n / (gn_ms * 1e-3),
+                      "backward_standin_ms": add_ms,
+                      "note": "gtc_step(grad=NULL) after the caller's backward accumulated into r: "
+                              "(r.add_(g) + gtc_step(NULL)) loop minus r.add_(g) loop, per step"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_oracle_run(n, tau, args.rho, args.cmp, args.alpha, args.cpu_seconds,
                              inputs=(grads_h, r0_h.copy(), w0_h.copy()), accum=args.accum, mu=args.mu)
-
-    value = world * n / (ms_per_step * 1e-3)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, args.warmup),
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": wl["desc"], "n_params": n, "tau": tau,
-                   "rho_target": args.rho, "rho_measured": k_rank / n, "cmp": args.cmp,
-                   "parallelism": f"dp{world}",
-                   "apply": f"ACCUM_MOMENTUM (mu={args.mu})" if momentum else "ACCUM_WEIGHTS",
-                   "exchange": ctx.exchange_mode(),
-                   "step": "one kernel" if one_kernel else "separate kernels",
-                   "l2": f"inputs larger than L2: g rotates over {NB} buffer(s), "
-                         f"g+r = {8 * n / 2**20:.0f} MiB per step vs 126 MB L2"},
-        "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": enc_gbs, "peak": peak,
-                     "unit": "GB/s", "frac": enc_gbs / peak, "traffic": traffic,
-                     "alg_bytes_per_launch": enc_bytes, "ms_per_launch": enc_ms,
-                     "peak_source": peak_src,
-                     "ms_per_launch_sampled_events": enc_ms_events,
-                     "share_of_step": enc_ms / ms_per_step,
-                     "nvlink_bytes_per_rank": nvl_bytes},
-        "kernels": {"encode_ms": enc_ms, "exchange_ms": exch_ms, "decode_apply_ms": dec_ms,
-                    "unfused_breakdown": brk,
-                    "decode_apply_GBs": dec_gbs, "decode_alg_bytes": dec_bytes, "nnz_counts": nnz_c,
-                    "k_per_rank": k_all,
-                    "step_alg_bytes": step_bytes,
-                    "step_hbm_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
-        "gpu_launches": launches,
-        "clocks": clocks.summary(),
-    }
     if e2e is not None:
         line["e2e"] = e2e
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+    ctx.close()  # collective at world > 1 (quiesce)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    ctx.close()
     return 0
 
 

@@ -109,13 +109,23 @@ enum { GTC_STEP_FUSED = 0,       /* default: the whole step is ONE kernel
  * contexts of ONE process (tests and single-process drivers; no NCCL
  * communicator, no CUDA IPC, nccl_unique_id must be NULL, p2p exchange,
  * world <= 8).  After every rank's gtc_bind_workspace, gtc_connect_loopback
- * links them.  A rank's gtc_exchange then launches a one-thread publish
- * kernel; the group steps either with the separate calls (every rank's
+ * links them.  A rank's gtc_encode then also launches a one-thread publish
+ * kernel (its ready flag); the group steps either with the separate calls (every rank's
  * gtc_encode, then every rank's gtc_exchange, then every rank's
  * gtc_decode_apply, in that order, so no kernel waits on one not yet queued)
  * or with gtc_step_group (the fused step of all ranks as ONE launch).
  * gtc_step on a loopback context returns GTC_EUNSUPPORTED. */
 enum { GTC_LOOPBACK = 64 };
+
+/* gtc_init flag (world 2..8, p2p): OWNER-COMPUTES decode:
+ * rank m owns tiles [ceil(m T / N), ceil((m+1) T / N)) of the T = ceil(n /
+ * GTC_TILE) tiles.  gtc_exchange counts the owned tiles from every rank's
+ * message (peer reads over NVLink) and publishes one sparse (index, count)
+ * list per tile; gtc_decode_apply applies every tile's list, read from its
+ * owner.  Per rank it reads (N-1)/N of each peer's message plus the other
+ * owners' lists instead of every peer's whole message.  gtc_step runs the
+ * three calls (no fused kernel).  Results are bit-identical to the default. */
+enum { GTC_DECODE_SHARDED = 128 };
 
 /* What decode_apply updates (R8, M1). */
 enum { GTC_ACCUM_WEIGHTS = 0, /* target[i] = fmaf(alpha, fl(c[i]*tau), target[i]) */
@@ -144,7 +154,8 @@ gtc_status gtc_get_unique_id(void* out_128_bytes);
  *  flags      : GTC_CMP_GT or GTC_CMP_GE, OR-ed with GTC_EXCHANGE_P2P (default) or
  *               GTC_EXCHANGE_NCCL, OR-ed with GTC_STEP_FUSED (default) or
  *               GTC_STEP_SPLIT, optionally OR-ed with GTC_LOOPBACK (then
- *               nccl_unique_id is NULL).  Other bits: GTC_EINVAL.
+ *               nccl_unique_id is NULL) and GTC_DECODE_SHARDED.  Other bits
+ *               or combinations: GTC_EINVAL.
  * The environment variable GTC_PEER_TIMEOUT_MS (read here) sets how long a
  * p2p kernel, or the NCCL-mode host wait, waits for a peer (default 30000).
  * On success *out is a new context (free with gtc_destroy). Blocks on NCCL

@@ -40,6 +40,7 @@ GTC_EXCHANGE_NCCL = 16
 GTC_STEP_FUSED = 0
 GTC_STEP_SPLIT = 32
 GTC_LOOPBACK = 64
+GTC_DECODE_SHARDED = 128
 GTC_ACCUM_WEIGHTS = 0
 GTC_ACCUM_UPDATE = 1
 GTC_ACCUM_MOMENTUM = 2
@@ -317,7 +318,7 @@ class GTC:
 
     def __init__(self, n_params: int, tau: float, rank: int = 0, world: int = 1, device=None,
                  cmp: str = "gt", max_words_per_rank: int = 0, max_sim_msgs: int = 0, group=None,
-                 exchange: str = "p2p", fused_step: bool = True, loopback: bool = False):
+                 exchange: str = "p2p", fused_step: bool = True, loopback: bool = False, sharded: bool = False):
         import torch
 
         if not torch.cuda.is_available():
@@ -330,6 +331,8 @@ class GTC:
         self.loopback = bool(loopback)
         if self.loopback:
             flags |= GTC_LOOPBACK
+        if sharded:
+            flags |= GTC_DECODE_SHARDED
         self.max_words = max_words_per_rank if max_words_per_rank > 0 else self.n
         uid = None
         if world > 1 and not self.loopback:
@@ -489,13 +492,13 @@ class LoopbackGroup:
     rank's exchange, then every rank's decode_apply (the separate calls)."""
 
     def __init__(self, n_params: int, tau: float, world: int, device=None, cmp: str = "gt",
-                 max_words_per_rank: int = 0):
+                 max_words_per_rank: int = 0, sharded: bool = False):
         import torch
 
         self.world = int(world)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.ranks = [GTC(n_params, tau, r, world, self.device, cmp=cmp, max_words_per_rank=max_words_per_rank,
-                          loopback=True) for r in range(world)]
+                          loopback=True, sharded=sharded) for r in range(world)]
         gtc_connect_loopback([g.ctx for g in self.ranks])
 
     def step(self, grads, residuals, targets, alpha: float = 1.0, mode: int = GTC_ACCUM_WEIGHTS,

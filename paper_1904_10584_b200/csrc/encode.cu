@@ -327,19 +327,20 @@ cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s) {
     return cmp_mode == GTC_CMP_GE ? launch_cmp<GTC_CMP_GE>(p, s) : launch_cmp<GTC_CMP_GT>(p, s);
 }
 
-// p2p loopback group (gtc_exchange): launched after the encode kernel on the
-// same stream.  The kernel boundary orders every encode store before this
-// kernel; one system-scope fence then makes them visible to the peers and the
-// release store raises this rank's ready flag, which peers acquire before
-// reading.  (Across processes the decode kernel's block 0 does the same at
-// its start, saving this launch.)
-__global__ void gtc_publish_kernel(Ctrl* ctrl, unsigned long long step) {
+// p2p loopback group (after gtc_encode) and the sharded decode (after the
+// owner count): launched after the producing kernel on the same stream.  The
+// kernel boundary orders every store of that kernel before this one; one
+// system-scope fence then makes them visible to the peers and the release
+// store raises the flag, which peers acquire before reading.  (Across
+// processes the decode kernel's block 0 raises the ready flag at its start,
+// saving this launch.)
+__global__ void gtc_publish_kernel(unsigned long long* flag, unsigned long long step) {
     __threadfence_system();
-    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(&ctrl->ready), "l"(step) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(flag), "l"(step) : "memory");
 }
 
-cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s) {
-    gtc_publish_kernel<<<1, 1, 0, s>>>(ctrl, step);
+cudaError_t launch_publish(unsigned long long* flag, unsigned long long step, cudaStream_t s) {
+    gtc_publish_kernel<<<1, 1, 0, s>>>(flag, step);
     return cudaGetLastError();
 }
 

@@ -51,9 +51,11 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 //   sim_off   i32[max_sim_msgs * (T + 1)]        tile offsets for decode_apply_msgs
 //   push[p][m] T records of kPushRec bytes        p2p: what rank m pushed (fused step), p < 2
 //   group     FusedStepParams[world]             loopback: the group launch's parameters
+//   ctags[p], clist[p]  { u64 tags[T] | u32 entries[T*kTile] }  sharded decode: count lists, p < 2
 struct Layout {
     int nseg;
     size_t ctrl, group_sum, seg_tags[2], seg_words[2];
+    size_t ctags[2], clist[2];
     size_t msg_hdr, msg_off, msg_words;
     size_t ipc, kx_all, recv, recv_off, sim_off;
     size_t push, push_slot;  // push[p][m] at push + (p * world + m) * push_slot
@@ -63,7 +65,8 @@ struct Layout {
 
 constexpr size_t kIpcRecord = kIpcRecordBytes;
 
-Layout make_layout(long long n, int world, bool p2p, bool loopback, long long capacity, int max_sim_msgs) {
+Layout make_layout(long long n, int world, bool p2p, bool loopback, bool sharded, long long capacity,
+                   int max_sim_msgs) {
     const long long tiles = (n + kTile - 1) / kTile;
     const size_t T = (size_t)std::max(tiles, 1LL);
     Layout L{};
@@ -99,6 +102,12 @@ Layout make_layout(long long n, int world, bool p2p, bool loopback, long long ca
     if (loopback) {
         L.group = o; o = align_up(o + sizeof(FusedStepParams) * (size_t)world, 256);
     }
+    for (int i = 0; i < 2; ++i) {
+        L.ctags[i] = L.clist[i] = 0;
+        if (!sharded) continue;
+        L.ctags[i] = o; o = align_up(o + sizeof(unsigned long long) * T, 256);
+        L.clist[i] = o; o = align_up(o + sizeof(unsigned) * T * kTile, 256);
+    }
     L.total = o;
     return L;
 }
@@ -113,6 +122,7 @@ struct gtc_ctx {
     int cmp_mode = GTC_CMP_GT;
     bool p2p = false;
     bool loopback = false;          // GTC_LOOPBACK: a rank of an in-process group (no NCCL, no IPC)
+    bool sharded = false;           // GTC_DECODE_SHARDED: owner-computes decode (sharded.cu)
     bool connected = false;         // loopback: gtc_connect_loopback done
     bool dead = false;              // the NCCL communicator was aborted (timeout)
     unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;  // p2p: longest wait for a peer
@@ -282,7 +292,10 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     if (!(tau > 0.f) || std::isinf(tau)) return GTC_EINVAL;
     if (world < 1 || rank < 0 || rank >= world) return GTC_EINVAL;
     if (world > GTC_MAX_MSGS) return GTC_EUNSUPPORTED;
-    if (flags & ~(uint32_t)(GTC_CMP_GE | GTC_EXCHANGE_NCCL | GTC_STEP_SPLIT | GTC_LOOPBACK)) return GTC_EINVAL;
+    if (flags & ~(uint32_t)(GTC_CMP_GE | GTC_EXCHANGE_NCCL | GTC_STEP_SPLIT | GTC_LOOPBACK | GTC_DECODE_SHARDED))
+        return GTC_EINVAL;
+    if ((flags & GTC_DECODE_SHARDED) && (world < 2 || (flags & GTC_EXCHANGE_NCCL) || world > kFusedMaxRanks))
+        return GTC_EINVAL;  // the owner-computes decode is a p2p mode of 2..8 ranks
     const bool loopback = (flags & GTC_LOOPBACK) != 0;
     if (loopback) {
         // an in-process group: no NCCL id, p2p exchange only
@@ -302,6 +315,7 @@ gtc_status gtc_init(gtc_ctx** out, int64_t n_params, float tau, int rank, int wo
     c->cmp_mode = (int)(flags & GTC_CMP_GE);
     c->p2p = world > 1 && !(flags & GTC_EXCHANGE_NCCL);
     c->loopback = loopback;
+    c->sharded = (flags & GTC_DECODE_SHARDED) != 0;
     c->split_step = (flags & GTC_STEP_SPLIT) != 0;
     if (const char* e = std::getenv("GTC_PEER_TIMEOUT_MS")) {
         const long long ms = std::atoll(e);
@@ -345,7 +359,7 @@ gtc_status gtc_workspace_size(const gtc_ctx* c, int64_t max_words_per_rank, int 
     if (!c || !bytes) return GTC_EINVAL;
     if (max_sim_msgs < 0 || max_sim_msgs > GTC_MAX_MSGS) return GTC_EINVAL;
     const long long cap = max_words_per_rank <= 0 ? c->n : std::min<long long>(max_words_per_rank, c->n);
-    *bytes = make_layout(c->n, c->world, c->p2p, c->loopback, cap, max_sim_msgs).total;
+    *bytes = make_layout(c->n, c->world, c->p2p, c->loopback, c->sharded, cap, max_sim_msgs).total;
     return GTC_OK;
 }
 
@@ -356,7 +370,7 @@ gtc_status gtc_bind_workspace(gtc_ctx* c, void* dev_ptr, size_t bytes, int64_t m
     if (reinterpret_cast<uintptr_t>(dev_ptr) & 255u) return fail(c, GTC_EALIGN, "workspace not 256-byte aligned");
     if (max_sim_msgs < 0 || max_sim_msgs > GTC_MAX_MSGS) return fail(c, GTC_EINVAL, "max_sim_msgs");
     const long long cap = max_words_per_rank <= 0 ? c->n : std::min<long long>(max_words_per_rank, c->n);
-    const Layout L = make_layout(c->n, c->world, c->p2p, c->loopback, cap, max_sim_msgs);
+    const Layout L = make_layout(c->n, c->world, c->p2p, c->loopback, c->sharded, cap, max_sim_msgs);
     if (bytes < L.total) return fail(c, GTC_EINVAL, "workspace too small");
     DeviceGuard g(c->device);
     unsigned char* b = static_cast<unsigned char*>(dev_ptr);
@@ -460,12 +474,64 @@ static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cu
     // p2p: the decode kernel raises ready when it starts (no publish launch)
     s = encode_launch(c, grad, residual, stream, fused_target, fused_alpha, fused_mode);
     if (s != GTC_OK) return s;
+    if (c->loopback) {
+        // loopback group: every rank's encode is queued before any rank's
+        // exchange/decode, so the flag goes up here (one one-thread kernel) --
+        // no kernel ever waits on one not yet queued
+        const cudaError_t e = launch_publish(&c->ctrl->ready, c->encodes, stream);
+        if (e != cudaSuccess) return cuda_fail(c, e, "encode: publish");
+        c->launches += 1;
+    }
     c->stage = Stage::kEncoded;
     return GTC_OK;
 }
 
 gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream) {
     return encode_impl(c, grad, residual, stream, nullptr, 0.f, GTC_ACCUM_WEIGHTS);
+}
+
+// Sharded decode (sharded.cu) parameters of the current step.
+static ShardParams shard_params(gtc_ctx* c) {
+    const int par = seg_parity(c);
+    ShardParams q{};
+    for (int i = 0; i < c->world; ++i) {
+        unsigned char* b = rank_ws(c, i);
+        Ctrl* ci = reinterpret_cast<Ctrl*>(b + c->L.ctrl);
+        q.seg[i] = reinterpret_cast<const unsigned*>(b + c->L.seg_words[par]);
+        q.tags[i] = reinterpret_cast<const unsigned long long*>(b + c->L.seg_tags[par]);
+        q.ready[i] = &ci->ready;
+        q.counted[i] = &ci->counted;
+        q.peer_flags[i] = &ci->flags;
+        q.clist_of[i] = reinterpret_cast<const unsigned*>(b + c->L.clist[par]);
+        q.ctags_of[i] = reinterpret_cast<const unsigned long long*>(b + c->L.ctags[par]);
+    }
+    q.clist = reinterpret_cast<unsigned*>(c->ws + c->L.clist[par]);
+    q.ctags = reinterpret_cast<unsigned long long*>(c->ws + c->L.ctags[par]);
+    q.nranks = c->world;
+    q.rank = c->rank;
+    q.n = c->n;
+    q.num_tiles = c->num_tiles;
+    q.epoch = c->epoch;
+    q.step = c->encodes;
+    q.timeout_ns = c->timeout_ns;
+    q.tau = c->tau;
+    q.flags = &c->ctrl->flags;
+    return q;
+}
+
+// gtc_exchange, sharded: the owner count of this rank's tiles (its block 0
+// raises this rank's ready flag first), then `counted` goes up.
+static gtc_status owner_count(gtc_ctx* c, cudaStream_t stream) {
+    ShardParams q = shard_params(c);
+    q.publish = &c->ctrl->ready;
+    cudaError_t e = launch_owner_count(q, stream);
+    if (e == cudaSuccess && c->num_tiles > 0) {
+        c->launches += 1;
+        e = launch_publish(&c->ctrl->counted, c->encodes, stream);
+        c->launches += 1;
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "exchange: owner count");
+    return GTC_OK;
 }
 
 static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
@@ -532,18 +598,17 @@ static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
 gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
     if (!c) return GTC_EINVAL;
     if (c->stage != Stage::kEncoded) return fail(c, GTC_ESTATE, "exchange: no encode since the last exchange");
+    if (c->sharded) {
+        DeviceGuard g(c->device);
+        gtc_status s = owner_count(c, stream);
+        if (s != GTC_OK) return s;
+        c->stage = Stage::kExchanged;
+        return GTC_OK;
+    }
     if (c->world == 1 || c->p2p) {
         // world 1: nothing to send.  p2p: decode_apply raises this rank's
-        // ready flag when it starts and reads the peers' tiles in place over
-        // NVLink once theirs are up.  Loopback group: every rank's decode is
-        // queued behind every rank's encode, so the flag goes up here (one
-        // one-thread kernel) -- no kernel ever waits on one not yet running.
-        if (c->loopback) {
-            DeviceGuard g(c->device);
-            const cudaError_t e = launch_publish(c->ctrl, c->encodes, stream);
-            if (e != cudaSuccess) return cuda_fail(c, e, "exchange: publish");
-            c->launches += 1;
-        }
+        // ready flag when it starts (loopback: gtc_encode did) and reads the
+        // peers' tiles in place over NVLink once theirs are up.
         c->stage = Stage::kExchanged;
         return GTC_OK;
     }
@@ -574,6 +639,18 @@ gtc_status gtc_bind_momentum(gtc_ctx* c, float* buf, float mu) {
 // every rank's ready flag).
 static gtc_status decode_launch(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
                                 cudaStream_t stream) {
+    if (c->sharded) {
+        ShardParams q = shard_params(c);
+        q.alpha = alpha;
+        q.target = target;
+        q.buf = c->mom_buf;
+        q.mu = c->mom_mu;
+        q.counts_out = reinterpret_cast<signed char*>(counts_out);
+        const cudaError_t e = launch_apply_counts(q, mode, stream);
+        if (e != cudaSuccess) return cuda_fail(c, e, "decode_apply: apply counts");
+        if (c->num_tiles > 0) c->launches += 1;
+        return GTC_OK;
+    }
     DecodeParams p{};
     if (c->world == 1 || c->p2p) {
         const int par = seg_parity(c);
@@ -731,8 +808,8 @@ gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* targe
         // queued: a loopback group steps with gtc_step_group, or with every
         // rank's encode, then exchange, then decode_apply
         return fail(c, GTC_EUNSUPPORTED, "step: loopback contexts step with gtc_step_group");
-    if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1 && !c->split_step && fused_step_enabled() &&
-        c->world <= kFusedMaxRanks) {
+    if (c && c->world > 1 && c->p2p && c->bound && c->num_tiles > 1 && !c->split_step && !c->sharded &&
+        fused_step_enabled() && c->world <= kFusedMaxRanks) {
         gtc_status s = check_encode_args(c, grad, residual);
         if (s == GTC_OK) s = check_apply_args(c, target, mode);
         if (s != GTC_OK) return s;

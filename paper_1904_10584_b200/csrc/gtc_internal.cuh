@@ -34,9 +34,8 @@ struct alignas(256) Ctrl {
     unsigned long long flags;     // sticky flags
     unsigned long long ready;     // p2p: the step (encodes since bind) whose message the
                                   // rank has published (separate calls)
-    unsigned long long counted;   // p2p sharded decode: the step whose owner counts the
-                                  // rank has published (Sec. f4)
-    unsigned long long arrive[2]; // p2p sharded decode: CTA arrival counters per parity
+    unsigned long long counted;   // p2p sharded decode: the step whose owner count lists
+                                  // the rank has published (sharded.cu)
 };
 
 // Header of a contiguous message region.
@@ -162,6 +161,45 @@ struct FusedStepParams {
     int trace;                                         // GTC_DECODE_TRACE=1: phase stamps (debug)
 };
 
+// Owner-computes (sharded) decode, GTC_DECODE_SHARDED (sharded.cu; SURVEY
+// 8(f) #4): rank m owns tiles [tile_begin(m), tile_begin(m + 1)) with
+// tile_begin(m) = ceil(m T / N).  gtc_exchange: the owner counts its tiles
+// from every rank's stamped entries (peer reads) and writes one COUNT LIST
+// per tile -- entries (local << 8) | (count & 0xff), ascending local index,
+// tag (epoch << 32) | length; gtc_decode_apply: every rank applies every
+// tile from its owner's list.
+__host__ __device__ __forceinline__ long long shard_tile_begin(int m, int nranks, long long tiles) {
+    return (m * tiles + nranks - 1) / nranks;
+}
+__host__ __device__ __forceinline__ int shard_owner(long long t, int nranks, long long tiles) {
+    return (int)((t * nranks) / tiles);
+}
+
+struct ShardParams {
+    const unsigned* seg[kFusedMaxRanks];               // every rank's stamped entries (this step's parity)
+    const unsigned long long* tags[kFusedMaxRanks];    // every rank's tile tags
+    const unsigned long long* ready[kFusedMaxRanks];   // every rank's Ctrl::ready
+    const unsigned long long* counted[kFusedMaxRanks]; // every rank's Ctrl::counted
+    unsigned long long* peer_flags[kFusedMaxRanks];    // every rank's Ctrl::flags (timeout broadcast)
+    unsigned long long* publish;                       // count: this rank's Ctrl::ready; apply: Ctrl::counted
+    unsigned* clist;                                   // this rank's count lists (this parity), [T * kTile]
+    unsigned long long* ctags;                         // this rank's count-list tags, [T]
+    const unsigned* clist_of[kFusedMaxRanks];          // every owner's count lists
+    const unsigned long long* ctags_of[kFusedMaxRanks];
+    int nranks, rank;
+    long long n;
+    int num_tiles;
+    unsigned epoch;
+    unsigned long long step;
+    unsigned long long timeout_ns;
+    float tau, alpha;
+    float* target;
+    float* buf;                                        // GTC_ACCUM_MOMENTUM
+    float mu;
+    signed char* counts_out;                           // may be null
+    unsigned long long* flags;                         // this rank's Ctrl::flags
+};
+
 struct BoundsParams {
     const unsigned int* words[GTC_MAX_MSGS];
     long long k[GTC_MAX_MSGS];
@@ -183,7 +221,9 @@ void ipc_unmap(std::vector<void*>& allocs);
 bool pdl_enabled();  // programmatic dependent launch (GTC_PDL=0 disables)
 cudaError_t launch_encode(EncodeParams& p, int cmp_mode, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& p, cudaStream_t s);
-cudaError_t launch_publish(Ctrl* ctrl, unsigned long long step, cudaStream_t s);
+cudaError_t launch_publish(unsigned long long* flag, unsigned long long step, cudaStream_t s);
+cudaError_t launch_owner_count(const ShardParams& p, cudaStream_t s);
+cudaError_t launch_apply_counts(const ShardParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_decode_apply(const DecodeParams& p, int accum_mode, cudaStream_t s);
 cudaError_t launch_tile_bounds(const BoundsParams& p, cudaStream_t s);
 cudaError_t launch_step_p2p(FusedStepParams& p, int cmp_mode, int accum_mode, cudaStream_t s);

@@ -165,8 +165,7 @@ def steady_residual(grads, tau: float, seed: int) -> np.ndarray:
     r0 = sign(sum_j g_j) * U(0, tau) (an element drifting up sits in (0, tau]
     between quanta), so the measured density equals sigma_for_cycle_density's
     target from the first step instead of after ~500 steps."""
-    d = np.zeros(grads[0].size, dtype=np.float64)
-    for g in grads:
-        d += g
+    d = grads[0] if len(grads) == 1 else np.sum(np.stack(grads), axis=0, dtype=np.float32)
     u = uniform(grads[0].size, 0.0, tau, seed)
-    return np.where(d < 0, -u, u).astype(np.float32)
+    np.negative(u, out=u, where=d < 0)
+    return u

@@ -37,7 +37,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=cmp, exchange=exchange)
+    sharded = os.environ.get("GTC_SHARDED") == "1"
+    ctx = gtc.GTC(n, tau, rank, world, dev, cmp=cmp, exchange=exchange, sharded=sharded)
     assert ctx.exchange_mode() == exchange, ctx.exchange_mode()
 
     r0 = [synth.uniform(n, -tau, tau, synth.rank_seed(w)) for w in range(world)]
@@ -105,7 +106,8 @@ def main():
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
-        print(f"MULTIGPU OK world={world} n={n} steps={steps} cmp={cmp} exchange={exchange} momentum={momentum}")
+        print(f"MULTIGPU OK world={world} n={n} steps={steps} cmp={cmp} exchange={exchange} momentum={momentum} "
+              f"sharded={sharded}")
 
 
 

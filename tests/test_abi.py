@@ -55,7 +55,7 @@ def test_host_side_validation_without_gpu():
     with pytest.raises(gtc.GTCError):
         gtc.gtc_init(10, 8.0, world=2)  # world > 1 needs a unique id
     with pytest.raises(gtc.GTCError) as e:
-        gtc.gtc_init(10, 8.0, flags=128)  # no such flag bit
+        gtc.gtc_init(10, 8.0, flags=256)  # no such flag bit
     assert e.value.status == gtc.GTC_EINVAL
     assert gtc.GTC_STEP_SPLIT & (gtc.GTC_CMP_GE | gtc.GTC_EXCHANGE_NCCL) == 0
     with pytest.raises(gtc.GTCError) as e:
@@ -63,6 +63,9 @@ def test_host_side_validation_without_gpu():
     assert e.value.status == gtc.GTC_EINVAL
     with pytest.raises(gtc.GTCError) as e:
         gtc.gtc_init(10, 8.0, world=2, unique_id=b"\0" * 128, flags=gtc.GTC_LOOPBACK)  # no NCCL id
+    assert e.value.status == gtc.GTC_EINVAL
+    with pytest.raises(gtc.GTCError) as e:  # the owner-computes decode needs >= 2 ranks
+        gtc.gtc_init(10, 8.0, world=1, flags=gtc.GTC_DECODE_SHARDED)
     assert e.value.status == gtc.GTC_EINVAL
     with pytest.raises(gtc.GTCError) as e:  # loopback exchanges p2p only
         gtc.gtc_init(10, 8.0, world=2, flags=gtc.GTC_LOOPBACK | gtc.GTC_EXCHANGE_NCCL)

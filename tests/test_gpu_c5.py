@@ -156,7 +156,9 @@ def run_c5(world):
     # SURVEY appendix (tau = 8, N(0,1) from r = 0): ~0 at step 1, 1.36 % at step 100
     assert dens[0] < 1e-8
     assert 0.009 < dens[-1] < 0.019, dens[-1]
-    assert dens[0] < dens[9] < dens[49] < dens[99]  # climbing while r fills up
+    # climbing while r fills up, then a plateau (measured: 1.3644 % at step 50,
+    # 1.3631 % at step 100)
+    assert dens[0] < dens[9] < dens[49] and abs(dens[99] - dens[49]) < 0.05 * dens[49]
     path = os.environ.get("GTC_C5_REPORT")
     if path:
         with open(path if world == 1 else path.replace(".json", f"_world{world}.json"), "w") as f:

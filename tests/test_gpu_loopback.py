@@ -7,9 +7,11 @@ one-GPU box: `world` contexts live in this process and every rank's peers are
 the other contexts' workspaces (plain device pointers instead of CUDA-IPC
 mappings).  The kernels are the production ones:
 
-  - split path: every rank's gtc_encode, gtc_exchange (loopback: the publish
-    kernel), then gtc_decode_apply -- the flag-gated decode reading the peers'
-    stamped tiles in place (no kernel ever waits on one not yet queued);
+  - split path: every rank's gtc_encode (loopback: followed by the publish
+    kernel), gtc_exchange, then gtc_decode_apply -- the flag-gated decode
+    reading the peers' stamped tiles in place (no kernel ever waits on one not
+    yet queued); with GTC_DECODE_SHARDED the owner count (gtc_exchange) and
+    the list apply (gtc_decode_apply);
   - fused path: gtc_step_group, the one-kernel encode -> push -> decode ->
     apply step of EVERY rank as ONE launch (rank r's CTA j is block j*world+r,
     so no launch waits on another launch).
@@ -64,9 +66,9 @@ def grads_for(kind, n, tau, t, world):
 class Run:
     """Device state of a loopback group plus the oracle's mirror of it."""
 
-    def __init__(self, n, tau, world, cmp, accum, mu=0.9, seed=0):
+    def __init__(self, n, tau, world, cmp, accum, mu=0.9, seed=0, sharded=False):
         self.n, self.tau, self.world, self.cmp, self.accum, self.mu = n, tau, world, cmp, accum, mu
-        self.grp = gtc.LoopbackGroup(n, tau, world, DEV, cmp=cmp)
+        self.grp = gtc.LoopbackGroup(n, tau, world, DEV, cmp=cmp, sharded=sharded)
         self.r_or = [synth.uniform(n, -tau, tau, synth.rank_seed(w), seed) for w in range(world)]
         self.w_or = synth.normal(n, 99 + seed)
         if accum == "update":
@@ -133,6 +135,49 @@ def test_loopback_split_parity(world, cmp, accum):
         om, oc, _ = run.oracle_step(gs, alpha)
         run.check(om, oc, f"split world={world} step {t}", counts)
     run.close()
+
+
+# ------------------------------------------------------------------ owner-computes (sharded) decode
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("accum", ["weights", "update", "momentum"])
+def test_loopback_sharded_parity(world, accum):
+    """GTC_DECODE_SHARDED: each owner counts its tile range
+    from every rank's message and publishes per-tile (index, count) lists;
+    every rank applies every list.  Bit-identical to the replicated decode and
+    the oracle, counts_out included (odd n: a ragged last tile)."""
+    n, tau, alpha = 1_000_003, 8.0, -0.5
+    run = Run(n, tau, world, "gt" if world != 3 else "ge", accum, sharded=True)
+    counts = [torch.empty(n, dtype=torch.int8, device=DEV) for _ in range(world)]
+    for t in range(4):
+        gs = grads_for("correlated" if t % 2 == 0 else "dense", n, tau, t, world)
+        run.zero_update_targets()
+        run.grp.split_step([to_dev(g) for g in gs], run.rd, run.wd, alpha, GMODE[accum], counts_out=counts)
+        torch.cuda.synchronize()
+        om, oc, _ = run.oracle_step(gs, alpha)
+        run.check(om, oc, f"sharded world={world} step {t}", counts)
+    # gtc_step on a sharded context of a loopback group is refused like any
+    # loopback gtc_step; without counts_out the sparse list apply runs
+    for t in range(4, 6):
+        gs = grads_for("correlated", n, tau, t, world)
+        run.zero_update_targets()
+        run.grp.split_step([to_dev(g) for g in gs], run.rd, run.wd, alpha, GMODE[accum])
+        torch.cuda.synchronize()
+        om, oc, _ = run.oracle_step(gs, alpha)
+        run.check(om, oc, f"sharded world={world} step {t} (no counts)")
+    run.close()
+
+
+def test_loopback_sharded_tiny_and_more_ranks_than_tiles():
+    """Owner ranges of 0 tiles (n < world tiles) and a one-tile vector."""
+    for n in (1, 4097, 3 * 4096 + 5):
+        run = Run(n, 2.0, 4, "gt", "weights", sharded=True)
+        for t in range(2):
+            gs = grads_for("correlated", n, 2.0, t, 4)
+            run.grp.split_step([to_dev(g) for g in gs], run.rd, run.wd, -0.5)
+            torch.cuda.synchronize()
+            om, oc, _ = run.oracle_step(gs, -0.5)
+            run.check(om, oc, f"sharded tiny n={n} step {t}")
+        run.close()
 
 
 # ------------------------------------------------------------------ fused one-kernel step

@@ -100,3 +100,18 @@ def test_unfused_step_parity():
            "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("world,accum", [(2, "weights"), (4, "update"), (4, "momentum")])
+def test_sharded_decode_multigpu(world, accum):
+    """GTC_DECODE_SHARDED across processes: owner counts over NVLink peer
+    reads, per-tile (index, count) lists, every rank applies every list."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, GTC_CMP="gt", GTC_STEPS="4", GTC_N="1000003", GTC_EXCHANGE="p2p", GTC_ACCUM=accum,
+               GTC_SHARDED="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29538", os.path.join(ROOT, "tests", "mp_gtc_worker.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "sharded=True" in p.stdout

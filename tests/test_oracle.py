@@ -371,6 +371,24 @@ def test_density_closed_form():
         assert abs(got - rho) / rho < 0.1, (rho, got)
 
 
+@pytest.mark.parametrize("nb,corr", [(3, 0.0), (1, 0.0), (3, 0.5)])
+def test_cycle_density_closed_form(nb, corr):
+    """The bench's input recipe: nb LSTM-shaped gradients applied in rotation
+    from synth.steady_residual; sigma_for_cycle_density's target density holds
+    from the first cycle on and stays (oracle encode, statistical)."""
+    n, tau, rho = 300_000, 8.0, 0.01
+    sigma = synth.sigma_for_cycle_density(rho, tau, synth.mean_abs_scale(n), nb, corr)
+    gs = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, t, 1, corr) for t in range(nb)]
+    r = synth.steady_residual(gs, tau, 5)
+    dens = []
+    for t in range(60):
+        words, _ = oracle.encode(gs[t % nb], r, tau)
+        dens.append(words.size / n)
+    for a in (0, 30):
+        got = float(np.mean(dens[a:a + 30]))
+        assert abs(got - rho) / rho < 0.1, (a, got)
+
+
 def test_determinism():
     g = synth.normal(100_000, 9) * np.float32(5)
     a, b = np.zeros(100_000, np.float32), np.zeros(100_000, np.float32)
