@@ -110,6 +110,8 @@ class ClockSampler:
         self.marks = []
 
     def start(self):
+        if os.environ.get("BENCH_NO_SMI"):  # diagnostics: no sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
@@ -272,6 +274,9 @@ class NvlinkCounters:
     def __init__(self, gpu_index):
         self.h = None
         self.err = None
+        if os.environ.get("BENCH_NO_NVML"):  # diagnostics: no counters
+            self.err = "disabled (BENCH_NO_NVML)"
+            return
         try:
             import pynvml
 
@@ -349,7 +354,7 @@ def run_gtc(args):
         ctx.exchange()
         ctx.decode_apply(w, args.alpha, amode)
 
-    for t in range(max(3, args.warmup)):
+    for t in range(3):  # the separate calls once (and the buffers of both step parities)
         step(t)
     torch.cuda.synchronize()
     stepf = ctx.stepper(grads, r, w, args.alpha, amode, stream)
@@ -373,14 +378,16 @@ def run_gtc(args):
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local_rank)
     clocks.start()
-    nvl = NvlinkCounters(local_rank)
     time.sleep(0.6)
+    # the W warm-up steps run right before the timed region
+    for t in range(max(3, args.warmup)):
+        stepf(t)
+    torch.cuda.synchronize()
     launches0 = ctx.kernel_launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark()
-    nvl0 = nvl.read()
     e_start.record(stream)
     for t in range(K):
         if t in ev:
@@ -396,7 +403,6 @@ def run_gtc(args):
             stepf(t)
     e_end.record(stream)
     torch.cuda.synchronize()
-    nvl1 = nvl.read()
     if world > 1:
         dist.barrier()
     clocks.mark()
@@ -413,6 +419,21 @@ def run_gtc(args):
     phases = None
     if inst:
         phases = [sum(ev[t][i].elapsed_time(ev[t][i + 1]) for t in inst) / len(inst) for i in range(3)]
+
+    # NVLink data counters (NVML) bracket a SEPARATE, untimed pass of K steps:
+    # an NVML NVLink field read stalls a running p2p job for ~10 ms
+    # (profiles/r02/nvml_stall: 130.1 us/step over 200 steps with the read
+    # inside the timed region, 75.8 without)
+    nv_delta, nvl_err = None, "world 1"
+    if world > 1:
+        nvl = NvlinkCounters(local_rank)
+        nvl0 = nvl.read()
+        if -allmax([-(1.0 if nvl0 is not None else 0.0)])[0] > 0.5:  # every rank reads them
+            for t in range(K):
+                stepf(t)
+            torch.cuda.synchronize()
+        nv_delta = NvlinkCounters.delta(nvl0, nvl.read())
+        nvl_err = nvl.err
 
     # density over the timed steps' regime (untimed: the inputs are
     # stationary, so the next M steps sample the same distribution)
@@ -576,7 +597,6 @@ def run_gtc(args):
                 "touched_elements": nnz_c, "touched_sectors": sectors_c,
                 "share_of_step": kern_ms / ms_per_step}
     if world > 1:
-        nv_delta = NvlinkCounters.delta(nvl0, nvl1)
         roofline["nvlink"] = {
             "bytes_per_step_per_rank": nvl_bytes if one_kernel else 4 * (world - 1) * max(k_all_mean),
             "frac_of_900GBs": (nvl_bytes if one_kernel else 4 * (world - 1) * max(k_all_mean))
@@ -585,8 +605,8 @@ def run_gtc(args):
             / (ms_per_step * 1e-3) / 770e9,
             "counters_timed_region": None if nv_delta is None else
             {kk: v / K for kk, v in nv_delta.items()},  # per step
-            "counters_note": "NVML NVLink data counters of rank 0's GPU over the timed region, per step"
-            if nv_delta is not None else (nvl.err or "unavailable")}
+            "counters_note": "NVML NVLink data counters of rank 0's GPU over a separate untimed pass of K steps, "
+                             "per step" if nv_delta is not None else (nvl_err or "unavailable")}
     gn_bytes = base - 4 * n + rmw  # grad = NULL: no 4 n gradient read
     line = {
         "metric": METRIC, "value": world * n / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,

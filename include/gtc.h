@@ -272,6 +272,27 @@ gtc_status gtc_message(gtc_ctx* ctx, int rank, const uint32_t** dev_words, int64
  * debugging; waits for the device).  max_words is the room at host_words. */
 gtc_status gtc_read_message(gtc_ctx* ctx, int rank, uint32_t* host_words, int64_t max_words, int64_t* k);
 
+/* Wire format of a SparseUpdate (host-only, no device
+ * work, callable without a GPU).  The hot path's words are (index << 1) | neg
+ * (R3: sorting words sorts indices); SPEC's interchange layout is
+ * bit 31 = sign (1 => -tau), bits 0..30 = index.  A serialized update is,
+ * little-endian: magic "GTCU" (4 bytes), dim (u64), tau (f32), word count
+ * (u32), then the SPEC-layout words (u32 each): 20 + 4 k bytes
+ * ("bytes per update == 4 x word count + 16" counts the header
+ * without the magic).
+ *  gtc_wire_pack  : words = k canonical words (index << 1 | neg), ascending,
+ *                   every index < dim < 2^31 (else GTC_ECORRUPT, GTC_EDIM);
+ *                   writes 20 + 4k bytes to out (out_bytes too small:
+ *                   GTC_EINVAL, *written = the size needed).
+ *  gtc_wire_unpack: the inverse; validates magic, sizes, dim < 2^31, tau
+ *                   finite > 0, indices < dim and strictly ascending
+ *                   (GTC_ECORRUPT otherwise); writes the canonical words
+ *                   (at most max_words, else GTC_EINVAL) and *k, *dim, *tau. */
+gtc_status gtc_wire_pack(const uint32_t* words, int64_t k, uint64_t dim, float tau, void* out,
+                         size_t out_bytes, size_t* written);
+gtc_status gtc_wire_unpack(const void* in, size_t in_bytes, uint32_t* words, int64_t max_words,
+                           int64_t* k, uint64_t* dim, float* tau);
+
 /* Wait for `stream`, then report and clear this rank's sticky device flags:
  * GTC_EPEER, GTC_ECAPACITY, GTC_ECORRUPT, GTC_ENONFINITE or GTC_OK.  A peer
  * timeout anywhere in a p2p step is raised in EVERY rank's flags, so every

@@ -66,6 +66,9 @@ _SIGS = {
     "gtc_message": (_i32, [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]),
     "gtc_read_message": (_i32, [_vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]),
     "gtc_check": (_i32, [_vp, _vp]),
+    "gtc_wire_pack": (_i32, [_vp, _i64, ctypes.c_uint64, _f32, _vp, _sz, ctypes.POINTER(_sz)]),
+    "gtc_wire_unpack": (_i32, [_vp, _sz, _vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_uint64),
+                               ctypes.POINTER(_f32)]),
     "gtc_connect_loopback": (_i32, [_vp, _i32]),
     "gtc_step_group": (_i32, [_vp, _i32, _vp, _vp, _vp, _f32, _i32, _u32, _vp]),
     "gtc_quiesce": (_i32, [_vp]),
@@ -211,6 +214,33 @@ def gtc_read_message(ctx, rank: int, max_words: int):
     _chk(load_library().gtc_read_message(ctx, rank, buf.ctypes.data_as(_vp), max_words, ctypes.byref(k)),
          "gtc_read_message", ctx)
     return buf[: k.value].copy()
+
+
+def gtc_wire_pack(words, dim: int, tau: float) -> bytes:
+    """SPEC.md:202 wire format ("GTCU", dim, tau, count, SPEC-layout words) of
+    canonical words (index << 1 | neg, numpy uint32, ascending)."""
+    import numpy as np
+
+    w = np.ascontiguousarray(words, dtype=np.uint32)
+    need = _sz()
+    lib = load_library()
+    lib.gtc_wire_pack(w.ctypes.data_as(_vp), w.size, dim, tau, None, 0, ctypes.byref(need))
+    out = ctypes.create_string_buffer(max(need.value, 1))
+    _chk(lib.gtc_wire_pack(w.ctypes.data_as(_vp), w.size, dim, tau, out, need.value, ctypes.byref(need)),
+         "gtc_wire_pack")
+    return out.raw[: need.value]
+
+
+def gtc_wire_unpack(blob: bytes):
+    """(canonical words numpy uint32, dim, tau) of a SPEC.md:202 serialized update."""
+    import numpy as np
+
+    n_max = max(0, (len(blob) - 20) // 4)
+    words = np.empty(max(n_max, 1), dtype=np.uint32)
+    k, dim, tau = _i64(), ctypes.c_uint64(), _f32()
+    _chk(load_library().gtc_wire_unpack(blob, len(blob), words.ctypes.data_as(_vp), n_max, ctypes.byref(k),
+                                        ctypes.byref(dim), ctypes.byref(tau)), "gtc_wire_unpack")
+    return words[: k.value].copy(), dim.value, tau.value
 
 
 def gtc_exchange_mode(ctx) -> int:
@@ -427,6 +457,10 @@ class GTC:
     def read_message(self, rank: int | None = None):
         """Host (numpy uint32) copy of a rank's message of the last step (any world)."""
         return gtc_read_message(self.ctx, self.rank if rank is None else rank, self.max_words)
+
+    def serialize_message(self, rank: int | None = None) -> bytes:
+        """A rank's message of the last step in SPEC.md:202's wire format."""
+        return gtc_wire_pack(self.read_message(rank), self.n, self.tau)
 
     def exchange_mode(self) -> str:
         m = gtc_exchange_mode(self.ctx)

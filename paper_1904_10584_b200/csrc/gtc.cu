@@ -765,12 +765,15 @@ static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, flo
     f.rank = c->rank;
     f.nranks = c->world;
     f.lag_groups = step_p2p_lag_groups(c->num_tiles, ranks_per_device);
+    step_p2p_lags(c->num_tiles, ranks_per_device, &f.lag_tiles, &f.lag_pf);
+    f.ticket = &c->ctrl->ticket;
     f.num_groups = (c->num_tiles + kDecGroup - 1) / kDecGroup;
     f.target = target;
     f.alpha = alpha;
     f.flags = &c->ctrl->flags;
     f.timeout_ns = c->timeout_ns;
     f.trace = decode_trace_enabled() ? 1 : 0;
+    f.diag = std::getenv("GTC_STEP_DIAG") ? std::atoi(std::getenv("GTC_STEP_DIAG")) : 0;
     return GTC_OK;
 }
 
@@ -1036,6 +1039,59 @@ gtc_status gtc_read_message(gtc_ctx* c, int rank, uint32_t* host_words, int64_t 
     cudaError_t e = cudaDeviceSynchronize();
     if (e == cudaSuccess && *k > 0) e = cudaMemcpy(host_words, dev, sizeof(uint32_t) * (size_t)*k, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(c, e, "read_message: copy");
+    return GTC_OK;
+}
+
+gtc_status gtc_wire_pack(const uint32_t* words, int64_t k, uint64_t dim, float tau, void* out,
+                         size_t out_bytes, size_t* written) {
+    if (!written || k < 0 || (k > 0 && !words)) return GTC_EINVAL;
+    if (dim >= (1ull << 31)) return GTC_EDIM;
+    if (!(tau > 0.f) || !std::isfinite(tau)) return GTC_EINVAL;
+    const size_t need = 20 + 4 * (size_t)k;
+    *written = need;
+    if (!out || out_bytes < need) return GTC_EINVAL;
+    for (int64_t j = 0; j < k; ++j) {
+        const uint32_t i = words[j] >> 1;
+        if (i >= dim || (j > 0 && i <= (words[j - 1] >> 1))) return GTC_ECORRUPT;
+    }
+    unsigned char* o = static_cast<unsigned char*>(out);
+    const uint32_t kk = (uint32_t)k;
+    std::memcpy(o, "GTCU", 4);
+    std::memcpy(o + 4, &dim, 8);  // the ABI's hosts are little-endian (x86-64, aarch64)
+    std::memcpy(o + 12, &tau, 4);
+    std::memcpy(o + 16, &kk, 4);
+    for (int64_t j = 0; j < k; ++j) {
+        const uint32_t w = ((words[j] & 1u) << 31) | (words[j] >> 1);  // SPEC: bit 31 = sign, bits 0..30 = index
+        std::memcpy(o + 20 + 4 * j, &w, 4);
+    }
+    return GTC_OK;
+}
+
+gtc_status gtc_wire_unpack(const void* in, size_t in_bytes, uint32_t* words, int64_t max_words, int64_t* k,
+                           uint64_t* dim, float* tau) {
+    if (!in || !k || !dim || !tau) return GTC_EINVAL;
+    const unsigned char* b = static_cast<const unsigned char*>(in);
+    if (in_bytes < 20 || std::memcmp(b, "GTCU", 4) != 0) return GTC_ECORRUPT;
+    uint64_t d;
+    float t;
+    uint32_t kk;
+    std::memcpy(&d, b + 4, 8);
+    std::memcpy(&t, b + 12, 4);
+    std::memcpy(&kk, b + 16, 4);
+    if (d >= (1ull << 31) || !(t > 0.f) || !std::isfinite(t) || in_bytes != 20 + 4 * (size_t)kk) return GTC_ECORRUPT;
+    if ((int64_t)kk > max_words || (kk > 0 && !words)) return GTC_EINVAL;
+    uint32_t prev = 0;
+    for (uint32_t j = 0; j < kk; ++j) {
+        uint32_t w;
+        std::memcpy(&w, b + 20 + 4 * (size_t)j, 4);
+        const uint32_t i = w & 0x7fffffffu;
+        if (i >= d || (j > 0 && i <= prev)) return GTC_ECORRUPT;
+        prev = i;
+        words[j] = (i << 1) | (w >> 31);
+    }
+    *k = kk;
+    *dim = d;
+    *tau = t;
     return GTC_OK;
 }
 

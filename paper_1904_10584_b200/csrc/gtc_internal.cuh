@@ -36,6 +36,8 @@ struct alignas(256) Ctrl {
                                   // rank has published (separate calls)
     unsigned long long counted;   // p2p sharded decode: the step whose owner count lists
                                   // the rank has published (sharded.cu)
+    unsigned ticket;              // fused step: next CTA ticket of the running launch (wraps to
+                                  // 0 after the launch's last CTA takes its ticket; step_p2p.cu)
 };
 
 // Header of a contiguous message region.
@@ -150,8 +152,12 @@ struct FusedStepParams {
     const unsigned char* push_in[kFusedMaxRanks];      // rank m's records in this rank's push region (null: self)
     int rank;
     int nranks;
-    int lag_groups;                                    // decode group = encode group - lag_groups
-    int num_groups;                                    // ceil(num_tiles / kDecGroup) (set by the launcher)
+    int lag_groups;                                    // grouped kernel: decode group = encode group - lag_groups
+    int num_groups;                                    // grouped kernel: ceil(num_tiles / kDecGroup) (launcher)
+    int lag_tiles;                                     // ticketed kernel: CTA b encodes tile b, decodes b - lag_tiles
+    int lag_pf;                                        // ticketed kernel: ... and prefetches the targets of b - lag_pf
+    unsigned* ticket;                                  // ticketed kernel: the launch's CTA ticket counter
+                                                       // (loopback group: rank 0's, shared by the group)
     float* target;
     float alpha;
     unsigned long long* flags;                         // this rank's Ctrl::flags
@@ -159,6 +165,8 @@ struct FusedStepParams {
     unsigned long long timeout_ns;                     // longest wait for a peer's tile
     int skip;                                          // loopback test hook: this rank does nothing
     int trace;                                         // GTC_DECODE_TRACE=1: phase stamps (debug)
+    int diag;                                          // GTC_STEP_DIAG (experiments only): 1 blockIdx roles,
+                                                       // 2 no target RMW, 4 no decode (results invalid)
 };
 
 // Owner-computes (sharded) decode, GTC_DECODE_SHARDED (sharded.cu; SURVEY
@@ -233,6 +241,7 @@ cudaError_t launch_step_p2p(FusedStepParams& p, int cmp_mode, int accum_mode, cu
 cudaError_t launch_step_p2p_group(const FusedStepParams* group, const FusedStepParams& host, int world,
                                   int cmp_mode, int accum_mode, cudaStream_t s);
 int step_p2p_lag_groups(int num_tiles, int ranks_per_device);
+void step_p2p_lags(int num_tiles, int ranks_per_device, int* lag_tiles, int* lag_pf);
 cudaError_t read_step_trace(unsigned long long* host, int max_entries);
 cudaError_t read_decode_trace(unsigned long long* host, int max_entries);
 bool decode_trace_enabled();

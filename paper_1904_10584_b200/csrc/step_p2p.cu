@@ -55,6 +55,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 namespace gtc {
@@ -448,6 +449,355 @@ __device__ __forceinline__ void decode_cta(const FusedStepParams& f, long long t
     }
 }
 
+// ------------------------------------------------------------ ticketed kernel
+// The default fused step.  CTA with ticket b encodes tile b (b < T) and
+// decodes tile d = b - L (0 <= d < T) of every rank; tickets [T, T + L) only
+// decode, tickets [0, L) only encode.  Ticket = the order in which CTAs start
+// (one atomicInc per CTA on the launch's counter, which wraps back to 0 when
+// the launch's last CTA takes its ticket), so a CTA only ever waits on tiles
+// encoded by CTAs that started before it, on every rank -- progress does not
+// depend on the order in which the hardware dispatches CTAs.
+//
+// Both halves' loads go out together: r and g of tile b, every rank's tag of
+// tile d and a speculative first block of each rank's entries (peers: their
+// pushed records, local memory).  The decode counts tile d in biased bytes
+// (0x80 + c, |c| <= 8: an integer add per entry never carries across bytes;
+// shared-memory atomics, order-free, so the counts are deterministic), issues
+// the target loads of the touched float4s, and the target stores go out after
+// the encode's entry stores and pushes, so the target round trip overlaps
+// them.  A CTA holds its slot for about one encode plus part of one round
+// trip; nothing waits on NVLink unless a rank is more than L tiles behind.
+constexpr int kOvPerThread = 4;     // overflow entry loads per thread per round
+
+__device__ __forceinline__ void count_biased(unsigned* cw, unsigned e) {
+    const unsigned idx = (e >> 1) & (kTile - 1);
+    const unsigned sh = 8u * (idx & 3u);
+    atomicAdd(cw + (idx >> 2), (e & 1u) ? (0u - (1u << sh)) : (1u << sh));
+}
+
+template <int CMP, bool HAS_G, int MODE>
+__device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b, long long trace_slot) {
+    __shared__ unsigned s_scan[kTileVec * kTileWarps];
+    __shared__ unsigned s_misc[2];
+    __shared__ __align__(16) unsigned s_cw[kTile / 4];  // biased byte counts of tile d (word v: elements 4v..4v+3)
+    __shared__ int s_k[kFusedMaxRanks];
+    __shared__ int s_flag;
+    __shared__ __align__(128) unsigned long long s_rec[kPushRec / 8];  // the encode's push record
+
+    const EncodeParams& p = f.enc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = f.nranks;
+    const long long T = p.num_tiles;
+    const long long te = b < T ? b : -1;       // tile encoded here
+    const long long td = b - f.lag_tiles;      // tile decoded here
+    const bool dec = td >= 0 && td < T && !(f.diag & 4);
+    const bool trace = f.trace && tid == 0 && trace_slot < kStepTraceCtas;
+    auto stamp_ph = [&](int ph) {
+        if (trace) g_step_trace[trace_slot * kStepTracePhases + ph] = now_ns();
+    };
+    stamp_ph(0);
+    if (trace) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_step_trace[trace_slot * kStepTracePhases + 5] = smid | (dec ? 1u << 16 : 0u) | (te < 0 ? 1u << 17 : 0u);
+    }
+    if (f.skip) return;  // loopback test hook: a rank that never shows up
+
+    auto tag_ptr = [&](int m, long long t) -> const unsigned long long* {
+        return f.push_in[m] ? reinterpret_cast<const unsigned long long*>(f.push_in[m] + t * kPushRec) : f.tags[m] + t;
+    };
+    auto entry_ptr = [&](int m, long long t, int j) -> const unsigned* {
+        if (f.push_in[m] && j < kPushCap) return reinterpret_cast<const unsigned*>(f.push_in[m] + t * kPushRec + 16) + j;
+        return f.seg[m] + t * kTile + j;
+    };
+
+    // ---- every load in flight at once
+    const long long base = te * kTile;
+    const bool full_tile = te >= 0 && base + kTile <= p.n;
+    unsigned prev_ld = 0u;
+    float4 rv[kTileVec], gv[kTileVec];
+    if (te >= 0) {
+        if (tid == kTileThreads - 1) prev_ld = ld_tag_count(p.tags + te);
+        load_tile<HAS_G>(p, base, full_tile, tid, rv, gv);
+    }
+    const int S = kTileThreads / N;  // speculative entries per rank: thread tid reads entry sj of rank sm
+    const int sm = tid / S, sj = tid - sm * S;
+    unsigned long long tagv = 0ull;
+    unsigned spec = 0u;
+    // prefetch stage (tile tp = b - lag_pf, lag_pf < lag_tiles): the targets
+    // this CTA's successors will read-modify-write are pulled into L2 now, so
+    // the apply of tile tp (lag_tiles - lag_pf tickets later) waits on an L2
+    // round trip, not an HBM one.  An entry carrying this step's stamp is
+    // always one of its tile's (tile_encode.cuh), so no tag is needed; a record
+    // not yet landed is simply not prefetched (a hint, never a wait).
+    const long long tp = b - f.lag_pf;
+    const bool pf = MODE != GTC_ACCUM_MOMENTUM && f.lag_pf > 0 && tp >= 0 && tp < T && sm < N;
+    unsigned pfe = 0u;
+    if (pf) pfe = ld_relaxed_sys(entry_ptr(sm, tp, sj));
+    if (dec) {
+        if (tid < N) tagv = ld_relaxed_sys(tag_ptr(tid, td));
+        if (sm < N) spec = ld_relaxed_sys(entry_ptr(sm, td, sj));
+        reinterpret_cast<uint4*>(s_cw)[tid] = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+    }
+
+    // ---- encode, rows a1-a3 and the tile scan's ballots
+    unsigned sel = 0u, neg = 0u, my_off[kTileVec];
+    if (te >= 0) {
+        bool nonfinite;
+        quantize<CMP, HAS_G>(rv, gv, p.tau, sel, neg, nonfinite);
+        store_residual(p, base, full_tile, tid, rv);
+        if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
+        tile_scan_ballots(sel, lane, warp, my_off, s_scan);
+    }
+    if (dec && tid < N) s_k[tid] = ((unsigned)(tagv >> 32) == p.epoch) ? (int)(unsigned)tagv : -1;
+    const unsigned stamp = entry_stamp(p.epoch);
+    if (pf && (pfe >> kStampShift) == stamp)
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(f.target + tp * kTile + ((pfe >> 1) & (kTile - 1))));
+    __syncthreads();
+    if (te >= 0 && warp == kTileWarps - 1) {
+        const unsigned incl = tile_scan_finish(lane, s_scan);
+        if (lane == 31) {
+            s_misc[0] = incl;
+            s_misc[1] = prev_ld;
+            if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);
+            if (te == 0) *p.k_next = 0ull;
+        }
+    }
+
+    // ---- decode tile d, rows a6-a7: wait until every rank's tag is this
+    // step's and every speculative entry below its count carries this step's
+    // stamp (a record's tag can land before its entries); rare at lag L
+    bool failed = false;
+    if (dec) {
+        unsigned long long t0ns = 0ull;
+        for (;;) {
+            const bool notready = tid < N && s_k[tid] < 0;
+            const bool unknown = sm < N && s_k[sm] < 0;
+            const bool stale = sm < N && sj < s_k[sm] && (spec >> kStampShift) != stamp;
+            if (!__syncthreads_or(notready || unknown || stale)) break;
+            if (tid == 0) {
+                // give up at the timeout, or at once if a peer timeout was
+                // already raised on this rank (no cascade of waves of timeouts)
+                const unsigned long long now = now_ns();
+                if (t0ns == 0ull) t0ns = now;
+                s_flag = (now - t0ns > f.timeout_ns || (ld_relaxed_sys(f.flags) & kFlagPeer)) ? 1 : 0;
+            }
+            __syncthreads();
+            if (s_flag) {
+                failed = true;
+                break;
+            }
+            __nanosleep(64);
+            if (notready) {
+                tagv = ld_relaxed_sys(tag_ptr(tid, td));
+                if ((unsigned)(tagv >> 32) == p.epoch) s_k[tid] = (int)(unsigned)tagv;
+            }
+            if (unknown || stale) spec = ld_relaxed_sys(entry_ptr(sm, td, sj));
+            __syncthreads();
+        }
+        stamp_ph(1);
+        if (!failed) {
+            if (sm < N && sj < s_k[sm]) count_biased(s_cw, spec);
+            // entries [S, k_m) of every rank (dense tiles); beyond kPushCap
+            // they come from the owner's buffer over NVLink
+            int OV = 0;
+            for (int m = 0; m < N; ++m) OV += max(0, s_k[m] - S);
+            const unsigned long long t_ov = OV ? now_ns() : 0ull;
+            for (int c0 = 0; c0 < OV && !failed; c0 += kOvPerThread * kTileThreads) {
+                unsigned ov[kOvPerThread];
+                const unsigned* a[kOvPerThread];
+                unsigned pend = 0u, have = 0u;
+#pragma unroll
+                for (int u = 0; u < kOvPerThread; ++u) {
+                    const int fo = c0 + tid + u * kTileThreads;
+                    a[u] = nullptr;
+                    if (fo < OV) {
+                        int m = 0, rem = fo;
+                        while (rem >= max(0, s_k[m] - S)) {
+                            rem -= max(0, s_k[m] - S);
+                            ++m;
+                        }
+                        a[u] = entry_ptr(m, td, S + rem);
+                        ov[u] = ld_relaxed_sys(a[u]);
+                        have |= 1u << u;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kOvPerThread; ++u)
+                    if (((have >> u) & 1u) && (ov[u] >> kStampShift) != stamp) pend |= 1u << u;
+                while (pend && !failed) {
+                    __nanosleep(64);
+#pragma unroll
+                    for (int u = 0; u < kOvPerThread; ++u)
+                        if ((pend >> u) & 1u) ov[u] = ld_relaxed_sys(a[u]);
+#pragma unroll
+                    for (int u = 0; u < kOvPerThread; ++u)
+                        if (((pend >> u) & 1u) && (ov[u] >> kStampShift) == stamp) pend &= ~(1u << u);
+                    if (pend && now_ns() - t_ov > f.timeout_ns) failed = true;
+                }
+#pragma unroll
+                for (int u = 0; u < kOvPerThread; ++u)
+                    if (((have >> u) & 1u) && !failed) count_biased(s_cw, ov[u]);
+            }
+        }
+    }
+    // every count (and s_misc) visible; a timed-out wait anywhere aborts the decode
+    failed = __syncthreads_or(failed) != 0;
+    const bool apply = dec && !failed && !(f.diag & 2);
+    if (dec && failed) raise_peer_error(f);
+    stamp_ph(2);
+
+    // ---- apply loads (row a8): float4 v = tid + 256 h of tile d is elements
+    // 4v..4v+3, counts in word v of s_cw
+    const long long db = td * kTile;
+    float4 tv[kTileVec], bv[kTileVec];
+    unsigned cw[kTileVec];
+    unsigned todo = 0u;
+    if (apply) {
+#pragma unroll
+        for (int h = 0; h < kTileVec; ++h) {
+            const int v = tid + h * kTileThreads;
+            cw[h] = s_cw[v];
+            const long long e0 = db + 4ll * v;
+            const bool full = e0 + 4 <= p.n;
+            if (MODE == GTC_ACCUM_MOMENTUM) {
+                if (full) {
+                    tv[h] = ld_v4(reinterpret_cast<const float4*>(f.target + e0));
+                    bv[h] = ld_v4(reinterpret_cast<const float4*>(p.buf + e0));
+                }
+                if (e0 < p.n) todo |= 1u << h;
+            } else if (cw[h] != 0x80808080u) {
+                todo |= 1u << h;
+                if (full) tv[h] = *reinterpret_cast<const float4*>(f.target + e0);
+            }
+        }
+    }
+
+    // ---- encode, rows a4-a5: entries (stamped) to this rank's slot and the
+    // push record, tag, then one bulk copy per peer
+    if (te >= 0) {
+        const unsigned total = s_misc[0], prev = s_misc[1];
+        unsigned* dst = p.seg + base;
+        unsigned* s_ent = reinterpret_cast<unsigned*>(s_rec + 2);
+        if (total != 0) {
+#pragma unroll
+            for (int j = 0; j < kTileVec; ++j) {
+                unsigned o = s_scan[j * kTileWarps + warp] + my_off[j];
+                const unsigned l0 = (unsigned)(j * kTileThreads + tid) * 4u;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if ((sel >> (4 * j + e)) & 1u) {
+                        const unsigned w = make_entry(stamp, l0 + e, (neg >> (4 * j + e)) & 1u);
+                        st_relaxed_sys(dst + o, w);
+                        if (o < (unsigned)kPushCap) s_ent[o] = w;
+                        ++o;
+                    }
+                }
+            }
+        }
+        for (unsigned o = total + tid; o < prev; o += kTileThreads) st_relaxed_sys(dst + o, 0u);
+        const unsigned clr = min(max(total, prev), (unsigned)kPushCap);
+        const unsigned clr4 = (clr + 3u) & ~3u;  // bulk copies move multiples of 16 bytes
+        for (unsigned o = total + tid; o < clr4; o += kTileThreads) s_ent[o] = 0u;
+        if (tid == 0) {
+            const unsigned long long tag = make_tag(p.epoch, total);
+            st_relaxed_sys(p.tags + te, tag);
+            s_rec[0] = tag;
+            s_rec[1] = 0ull;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> the bulk copies
+    }
+    __syncthreads();
+    if (te >= 0 && tid == 0 && !(f.diag & 16)) {
+        const unsigned clr = min(max(s_misc[0], s_misc[1]), (unsigned)kPushCap);
+        const unsigned bytes = 16u + 4u * ((clr + 3u) & ~3u);
+#pragma unroll
+        for (int m = 0; m < kFusedMaxRanks; ++m) {
+            if (m >= N || !f.push_out[m]) continue;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         :: "l"(f.push_out[m] + te * kPushRec), "r"(smem_u32(s_rec)), "r"(bytes) : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+
+    stamp_ph(3);
+    // ---- apply stores: u = fl(c * tau); WEIGHTS fmaf(alpha, u, t), UPDATE
+    // fl(t + u) (R8) on the touched elements; MOMENTUM (M1) on every element
+    if (apply) {
+#pragma unroll
+        for (int h = 0; h < kTileVec; ++h) {
+            if (!((todo >> h) & 1u)) continue;
+            const long long e0 = db + 4ll * (tid + h * kTileThreads);
+            const int cc[4] = {(int)(cw[h] & 0xffu) - 128, (int)((cw[h] >> 8) & 0xffu) - 128,
+                               (int)((cw[h] >> 16) & 0xffu) - 128, (int)(cw[h] >> 24) - 128};
+            if (MODE == GTC_ACCUM_MOMENTUM) {
+                auto mom = [&](float& w, float& bf, int c) {
+                    const float u = __fmul_rn((float)c, p.tau);
+                    bf = __fadd_rn(__fmul_rn(p.mu, bf), u);
+                    w = __fmaf_rn(f.alpha, bf, w);
+                };
+                if (e0 + 4 <= p.n) {
+                    mom(tv[h].x, bv[h].x, cc[0]);
+                    mom(tv[h].y, bv[h].y, cc[1]);
+                    mom(tv[h].z, bv[h].z, cc[2]);
+                    mom(tv[h].w, bv[h].w, cc[3]);
+                    st_stream(reinterpret_cast<float4*>(f.target + e0), tv[h]);
+                    st_stream(reinterpret_cast<float4*>(p.buf + e0), bv[h]);
+                } else {
+                    for (int e = 0; e < 4 && e0 + e < p.n; ++e) mom(f.target[e0 + e], p.buf[e0 + e], cc[e]);
+                }
+            } else if (e0 + 4 <= p.n) {
+                float4 t = tv[h];
+                if (cc[0]) t.x = apply_count<MODE>(t.x, cc[0], p.tau, f.alpha);
+                if (cc[1]) t.y = apply_count<MODE>(t.y, cc[1], p.tau, f.alpha);
+                if (cc[2]) t.z = apply_count<MODE>(t.z, cc[2], p.tau, f.alpha);
+                if (cc[3]) t.w = apply_count<MODE>(t.w, cc[3], p.tau, f.alpha);
+                *reinterpret_cast<float4*>(f.target + e0) = t;
+            } else {
+                for (int e = 0; e < 4 && e0 + e < p.n; ++e)
+                    if (cc[e]) f.target[e0 + e] = apply_count<MODE>(f.target[e0 + e], cc[e], p.tau, f.alpha);
+            }
+        }
+    }
+    if (te >= 0 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    stamp_ph(4);
+}
+
+// The ticket of this CTA (one atomicInc; the counter wraps to 0 with the
+// launch's last ticket).  The atomic is performed before griddepcontrol's
+// launch_dependents, so a dependent launch on the stream (the next step) only
+// takes tickets after every ticket of this launch is taken.
+__device__ __forceinline__ unsigned take_ticket(unsigned* counter, unsigned last) {
+    __shared__ unsigned s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicInc(counter, last);
+    __syncthreads();
+    return s_ticket;
+}
+
+template <int CMP, bool HAS_G, int MODE>
+__global__ void __launch_bounds__(kTileThreads, 4) gtc_step_ticket_kernel(const FusedStepParams f) {
+    const unsigned b = (f.diag & 1) ? blockIdx.x : take_ticket(f.ticket, gridDim.x - 1u);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    ticket_cta<CMP, HAS_G, MODE>(f, b, b);
+}
+
+// Loopback group: one ticket sequence for the whole group (rank 0's
+// counter); ticket g is CTA g / world of rank g % world, so every tile a CTA
+// waits on (a lower CTA index of any rank) belongs to a lower ticket.
+template <int CMP, bool HAS_G, int MODE>
+__global__ void __launch_bounds__(kTileThreads, 4)
+gtc_step_ticket_group_kernel(const FusedStepParams* __restrict__ group, int world) {
+    __shared__ FusedStepParams s_f;
+    const unsigned g = take_ticket(group[0].ticket, gridDim.x - 1u);
+    const int rank = (int)(g % (unsigned)world);
+    const int* src = reinterpret_cast<const int*>(group + rank);
+    int* dst = reinterpret_cast<int*>(&s_f);
+    for (int i = threadIdx.x; i < (int)(sizeof(FusedStepParams) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    ticket_cta<CMP, HAS_G, MODE>(s_f, g / (unsigned)world, g);
+}
+
 // CTA b of one rank's step.
 template <int CMP, bool HAS_G, int MODE>
 __device__ __forceinline__ void step_cta(const FusedStepParams& f, long long b, long long trace_slot) {
@@ -517,11 +867,24 @@ gtc_step_p2p_group_kernel(const FusedStepParams* __restrict__ group, int world) 
     step_cta<CMP, HAS_G, MODE>(s_f, blockIdx.x / (unsigned)world, blockIdx.x);
 }
 
+// GTC_STEP_KERNEL=grouped: the previous design (groups of encode CTAs and a
+// decode CTA, roles by blockIdx), kept for comparison
+bool grouped_kernel() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_STEP_KERNEL");
+        v = (e && std::strcmp(e, "grouped") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 template <int CMP, bool HAS_G, int MODE>
 cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     const long long Q = f.num_groups;
-    cfg.gridDim = dim3((unsigned)(Q * (kDecGroup + 1) + std::min<long long>(f.lag_groups, Q)));
+    const bool grouped = grouped_kernel();
+    cfg.gridDim = grouped ? dim3((unsigned)(Q * (kDecGroup + 1) + std::min<long long>(f.lag_groups, Q)))
+                          : dim3((unsigned)(f.enc.num_tiles + f.lag_tiles));
     cfg.blockDim = dim3(kTileThreads);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -529,7 +892,8 @@ cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gtc_step_p2p_kernel<CMP, HAS_G, MODE>, f);
+    if (grouped) return cudaLaunchKernelEx(&cfg, gtc_step_p2p_kernel<CMP, HAS_G, MODE>, f);
+    return cudaLaunchKernelEx(&cfg, gtc_step_ticket_kernel<CMP, HAS_G, MODE>, f);
 }
 
 template <int CMP, bool HAS_G>
@@ -542,8 +906,14 @@ cudaError_t launch_g(FusedStepParams& f, int mode, cudaStream_t s) {
 template <int CMP, bool HAS_G, int MODE>
 cudaError_t launch_group_t(const FusedStepParams* group, const FusedStepParams& h, int world, cudaStream_t s) {
     const long long Q = h.num_groups;
-    const long long per_rank = Q * (kDecGroup + 1) + std::min<long long>(h.lag_groups, Q);
-    gtc_step_p2p_group_kernel<CMP, HAS_G, MODE><<<(unsigned)(per_rank * world), kTileThreads, 0, s>>>(group, world);
+    if (grouped_kernel()) {
+        const long long per_rank = Q * (kDecGroup + 1) + std::min<long long>(h.lag_groups, Q);
+        gtc_step_p2p_group_kernel<CMP, HAS_G, MODE><<<(unsigned)(per_rank * world), kTileThreads, 0, s>>>(group, world);
+    } else {
+        const long long per_rank = h.enc.num_tiles + h.lag_tiles;
+        gtc_step_ticket_group_kernel<CMP, HAS_G, MODE><<<(unsigned)(per_rank * world), kTileThreads, 0, s>>>(group,
+                                                                                                          world);
+    }
     return cudaGetLastError();
 }
 
@@ -578,6 +948,42 @@ int step_p2p_lag_groups(int num_tiles, int ranks_per_device) {
     const int groups = (num_tiles + kDecGroup - 1) / kDecGroup;
     const int lag = (w + kDecGroup) / (kDecGroup + 1);  // groups of G + 1 CTAs per wave
     return std::max(1, std::min(lag, groups));
+}
+
+// Ticketed kernel: decode lag in tiles, one wave of resident CTAs of one rank
+// (GTC_FUSED_LAG, in tiles, overrides).
+static int ticket_wave() {
+    static std::once_flag once;
+    static int wave = 592;
+    std::call_once(once, [] {
+        int dev = 0, sms = 0, per_sm = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, gtc_step_ticket_kernel<GTC_CMP_GT, true, GTC_ACCUM_WEIGHTS>, kTileThreads, 0) == cudaSuccess &&
+            sms > 0 && per_sm > 0)
+            wave = sms * per_sm;
+    });
+    return wave;
+}
+
+static int env_tiles(const char* name, int dflt) {  // read per step: tests vary them
+    const char* e = std::getenv(name);
+    return (e && e[0]) ? std::atoi(e) : dflt;
+}
+
+// Ticketed kernel lags (tiles).  Decode lag: the prefetch lag plus half a
+// wave (about one HBM round trip of the step's progress), GTC_FUSED_LAG
+// overrides.  Prefetch lag: one wave of resident CTAs of one rank,
+// GTC_PREFETCH_LAG overrides (0 = no prefetch stage), always below the decode
+// lag.
+void step_p2p_lags(int num_tiles, int ranks_per_device, int* lag_tiles, int* lag_pf) {
+    const int w = std::max(1, ticket_wave() / std::max(1, ranks_per_device));
+    int lp = env_tiles("GTC_PREFETCH_LAG", w);
+    const int la = std::max(1, env_tiles("GTC_FUSED_LAG", lp > 0 ? lp + w / 2 : w));
+    lp = std::max(0, std::min(lp, la - 1));
+    *lag_tiles = std::min(la, num_tiles + lp);
+    *lag_pf = std::min(lp, num_tiles);
 }
 
 cudaError_t read_step_trace(unsigned long long* host, int max_entries) {
