@@ -18,7 +18,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgtc.so")
+LIB_PATH = os.environ.get("GTC_LIB") or os.path.join(_PKG, "libgtc.so")  # GTC_LIB: experiment builds
 
 GTC_OK = 0
 GTC_EINVAL = 1

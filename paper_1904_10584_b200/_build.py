@@ -25,23 +25,25 @@ def sources():
         glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "gtc.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile every csrc/*.cu into `out` (default: the in-tree libgtc.so);
+    `defines` (-D flags) only for experiment builds (tools/build_variant.py)."""
     srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
     newest = max(os.path.getmtime(s) for s in sources())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
+    if not force and not defines and os.path.exists(out) and os.path.getmtime(out) >= newest:
+        return out
     nccl = _nccl_root()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
            "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
            f"-Xlinker=-rpath={os.path.join(nccl, 'lib')}",
-           "-o", LIB + ".tmp", *srcs]
+           *[f"-D{d}" for d in defines], "-o", out + ".tmp", *srcs]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

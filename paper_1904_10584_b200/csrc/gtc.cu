@@ -723,6 +723,9 @@ static bool fused_step_enabled() {
 // step of this parity was not fused.
 static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
                              cudaStream_t stream, int ranks_per_device, FusedStepParams& f) {
+    // GTC_STEP_PULL=1 (experiment): no pushed records, decoders read the
+    // peers' tags and entries in place over NVLink
+    const bool pull = std::getenv("GTC_STEP_PULL") && std::getenv("GTC_STEP_PULL")[0] == '1';
     begin_step(c);
     const int par = seg_parity(c);
     f = FusedStepParams{};
@@ -749,7 +752,7 @@ static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, flo
         f.peer_flags[i] = &reinterpret_cast<Ctrl*>(b + c->L.ctrl)->flags;
         f.push_out[i] = nullptr;
         f.push_in[i] = nullptr;
-        if (i == c->rank) continue;
+        if (i == c->rank || pull) continue;
         // this rank's records in rank i's push region, and rank i's in ours
         unsigned char* out = b + c->L.push + ((size_t)par * c->world + c->rank) * c->L.push_slot;
         if (!c->push_clean[par]) {
@@ -761,7 +764,7 @@ static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, flo
         f.push_out[i] = out;
         f.push_in[i] = c->ws + c->L.push + ((size_t)par * c->world + i) * c->L.push_slot;
     }
-    c->push_clean[par] = true;
+    c->push_clean[par] = !pull;
     f.rank = c->rank;
     f.nranks = c->world;
     f.lag_groups = step_p2p_lag_groups(c->num_tiles, ranks_per_device);

@@ -157,7 +157,8 @@ struct FusedStepParams {
     int lag_tiles;                                     // ticketed kernel: CTA b encodes tile b, decodes b - lag_tiles
     int lag_pf;                                        // ticketed kernel: ... and prefetches the targets of b - lag_pf
     unsigned* ticket;                                  // ticketed kernel: the launch's CTA ticket counter
-                                                       // (loopback group: rank 0's, shared by the group)
+                                                       // (loopback group: rank 0's, shared by the group);
+                                                       // warp-specialized kernel: its encode ticket counter
     float* target;
     float alpha;
     unsigned long long* flags;                         // this rank's Ctrl::flags

@@ -57,6 +57,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 namespace gtc {
 namespace {
@@ -775,7 +776,10 @@ __device__ __forceinline__ unsigned take_ticket(unsigned* counter, unsigned last
 }
 
 template <int CMP, bool HAS_G, int MODE>
-__global__ void __launch_bounds__(kTileThreads, 4) gtc_step_ticket_kernel(const FusedStepParams f) {
+#ifndef GTC_TICKET_CTAS
+#define GTC_TICKET_CTAS 4
+#endif
+__global__ void __launch_bounds__(kTileThreads, GTC_TICKET_CTAS) gtc_step_ticket_kernel(const FusedStepParams f) {
     const unsigned b = (f.diag & 1) ? blockIdx.x : take_ticket(f.ticket, gridDim.x - 1u);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
@@ -786,7 +790,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) gtc_step_ticket_kernel(const 
 // counter); ticket g is CTA g / world of rank g % world, so every tile a CTA
 // waits on (a lower CTA index of any rank) belongs to a lower ticket.
 template <int CMP, bool HAS_G, int MODE>
-__global__ void __launch_bounds__(kTileThreads, 4)
+__global__ void __launch_bounds__(kTileThreads, GTC_TICKET_CTAS)
 gtc_step_ticket_group_kernel(const FusedStepParams* __restrict__ group, int world) {
     __shared__ FusedStepParams s_f;
     const unsigned g = take_ticket(group[0].ticket, gridDim.x - 1u);
@@ -867,6 +871,624 @@ gtc_step_p2p_group_kernel(const FusedStepParams* __restrict__ group, int world) 
     step_cta<CMP, HAS_G, MODE>(s_f, blockIdx.x / (unsigned)world, blockIdx.x);
 }
 
+// ------------------------------------------------------------ warp-specialized kernel
+// The default fused step (WEIGHTS / UPDATE).  A persistent grid of two CTAs
+// per SM, each with kWsGroups ENCODE GROUPS of 256 threads and kWsDecWarps
+// DECODE WARPS.  Why: in every one-CTA-per-tile design the decode's latency-bound
+// round trips sit inside the CTAs that also carry the encode's HBM stream, so
+// they take slot time the stream needs (encode alone 55 us,
+// + pushes 61, + counting 69, + apply 76 us at N=2).  Here the encode groups
+// only stream (the register-load tile encode, 4 tiles in flight per SM, as in
+// the world-1 kernel) and the decode warps, outside that budget, follow the
+// encode by about one wave with two tiles in flight each.
+//   encode group: takes tickets (atomicInc, the next one taken while the
+//     current tile is processed) over (rank, tile) pairs and encodes the tile
+//     exactly as ticket_cta: stamped entries + tag (relaxed system-scope
+//     stores) and the record pushed to every peer by one bulk copy each.
+//   decode warp: decodes (rank, tile) tickets gw, gw + W, ... (W decode warps
+//     in the grid), which the encode front reaches in that order; for tile d of rank r
+//     it polls every rank's tag (peers: the pushed records, local memory),
+//     validates the speculative entries by their stamps, counts them in a
+//     warp-private biased-byte array (shared-memory atomics: order-free,
+//     deterministic), and read-modify-writes the touched float4s of the
+//     target (R8).  The next tile's tags and entries are loaded before the
+//     current tile's target round trip.
+// Progress: an encode never waits, and every tile is encoded by whichever
+// groups are running (tickets), so a waiting decode warp always waits on
+// work that is in progress on some rank -- no assumption on which CTAs are
+// resident.  A loopback group (R ranks of one process) runs every rank's
+// tickets in every CTA (ticket g = rank g % R, tile g / R).
+#ifndef GTC_WS_GROUPS
+#define GTC_WS_GROUPS 2
+#endif
+#ifndef GTC_WS_DECW
+#define GTC_WS_DECW 2
+#endif
+#ifndef GTC_WS_CTAS
+#define GTC_WS_CTAS 2
+#endif
+constexpr int kWsGroups = GTC_WS_GROUPS;   // encode groups per CTA
+constexpr int kWsDecWarps = GTC_WS_DECW;   // decode warps per CTA
+constexpr int kWsCtasPerSm = GTC_WS_CTAS;  // resident CTAs per SM (launch bounds)
+constexpr int kWsThreads = kWsGroups * kTileThreads + kWsDecWarps * 32;
+constexpr int kWsSpec = 8;  // speculative entry loads per decode lane per tile
+constexpr int kWsDecSmem = 4 * (kTile / 4 + 2 * 32 * kWsSpec + 32);  // dynamic smem per decode warp
+constexpr int kWsBatch = 4; // target float4 loads in flight per decode lane
+constexpr int kWsTraceTiles = 24;                       // debug trace: tiles per decode warp 0
+constexpr long long kWsTraceBase = 2048ll * kStepTracePhases;  // ... after the CTA slots
+
+struct alignas(128) WsGroupSmem {
+    unsigned long long rec[kPushRec / 8];  // the encode's push record (bulk copy source)
+    unsigned scan[kTileVec * kTileWarps];
+    unsigned misc[2];
+    unsigned ticket;
+};
+
+__device__ __forceinline__ void group_bar(int g) {
+    asm volatile("bar.sync %0, %1;" :: "r"(g + 1), "n"(kTileThreads) : "memory");
+}
+
+// One tile of an encode group (rows a1-a5 + the push), as ticket_cta's encode.
+// `nxt` (leader only) is the group's next ticket, published to the group here.
+template <int CMP, bool HAS_G>
+__device__ __forceinline__ unsigned ws_encode_tile(const FusedStepParams& f, long long t, int g, int gt,
+                                                   WsGroupSmem& G, unsigned nxt) {
+    const EncodeParams& p = f.enc;
+    const int lane = gt & 31, lw = gt >> 5;
+    const long long base = t * kTile;
+    const bool full_tile = base + kTile <= p.n;
+    unsigned prev_ld = 0u;
+    if (gt == kTileThreads - 1) prev_ld = ld_tag_count(p.tags + t);
+    float4 rv[kTileVec], gv[kTileVec];
+    load_tile<HAS_G>(p, base, full_tile, gt, rv, gv);
+    unsigned sel, neg;
+    bool nonfinite;
+    quantize<CMP, HAS_G>(rv, gv, p.tau, sel, neg, nonfinite);
+    store_residual(p, base, full_tile, gt, rv);
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&p.ctrl->flags, kFlagNonFinite);
+    unsigned my_off[kTileVec];
+    tile_scan_ballots(sel, lane, lw, my_off, G.scan);
+    group_bar(g);
+    if (lw == kTileWarps - 1) {
+        const unsigned incl = tile_scan_finish(lane, G.scan);
+        if (lane == 31) {
+            G.misc[0] = incl;
+            G.misc[1] = prev_ld;
+            if (incl) atomicAdd(p.k_acc, (unsigned long long)incl);
+            if (t == 0) *p.k_next = 0ull;
+        }
+    }
+    group_bar(g);
+    const unsigned total = G.misc[0], prev = G.misc[1];
+    const unsigned stamp = entry_stamp(p.epoch);
+    unsigned* dst = p.seg + base;
+    unsigned* s_ent = reinterpret_cast<unsigned*>(G.rec + 2);
+    if (total != 0) {
+#pragma unroll
+        for (int j = 0; j < kTileVec; ++j) {
+            unsigned o = G.scan[j * kTileWarps + lw] + my_off[j];
+            const unsigned l0 = (unsigned)(j * kTileThreads + gt) * 4u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if ((sel >> (4 * j + e)) & 1u) {
+                    const unsigned w = make_entry(stamp, l0 + e, (neg >> (4 * j + e)) & 1u);
+                    st_relaxed_sys(dst + o, w);
+                    if (o < (unsigned)kPushCap) s_ent[o] = w;
+                    ++o;
+                }
+            }
+        }
+    }
+    for (unsigned o = total + gt; o < prev; o += kTileThreads) st_relaxed_sys(dst + o, 0u);
+    const unsigned clr = min(max(total, prev), (unsigned)kPushCap);
+    const unsigned clr4 = (clr + 3u) & ~3u;  // bulk copies move multiples of 16 bytes
+    for (unsigned o = total + gt; o < clr4; o += kTileThreads) s_ent[o] = 0u;
+    if (gt == 0) {
+        const unsigned long long tag = make_tag(p.epoch, total);
+        st_relaxed_sys(p.tags + t, tag);
+        G.rec[0] = tag;
+        G.rec[1] = 0ull;
+        G.ticket = nxt;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> the bulk copies
+    group_bar(g);
+    const unsigned next = G.ticket;
+    if (gt == 0) {
+        const unsigned bytes = 16u + 4u * clr4;
+        for (int m = 0; m < f.nranks; ++m) {
+            if (!f.push_out[m]) continue;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         :: "l"(f.push_out[m] + t * kPushRec), "r"(smem_u32(G.rec)), "r"(bytes) : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // the record buffer is rewritten by the group's next tile
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    return next;
+}
+
+// The decode warp's messages of one tile: every rank's tag in lane m < N's
+// register, and the first S = (32 kWsSpec / N) & ~3 entries of every rank
+// (flat index m S + j) copied by cp.async into the warp's shared buffer --
+// no register holds an in-flight entry, so nothing spills and no copy waits
+// for another (a register spill of a loaded value serialises the loads).
+constexpr int kWsSlots = 32 * kWsSpec;  // entry slots per buffer
+// NR: the rank count rounded up to 2, 4 or 8 (a template parameter: the
+// window S = kWsSlots / NR and every slot's rank are compile-time constants)
+__host__ __device__ constexpr int ws_nr(int N) { return N <= 2 ? 2 : N <= 4 ? 4 : 8; }
+
+__device__ __forceinline__ const unsigned long long* ws_tag_ptr(const FusedStepParams& f, int m, long long t) {
+    return f.push_in[m] ? reinterpret_cast<const unsigned long long*>(f.push_in[m] + t * kPushRec) : f.tags[m] + t;
+}
+__device__ __forceinline__ const unsigned* ws_entry_ptr(const FusedStepParams& f, int m, long long t, int j) {
+    if (f.push_in[m] && j < kPushCap) return reinterpret_cast<const unsigned*>(f.push_in[m] + t * kPushRec + 16) + j;
+    return f.seg[m] + t * kTile + j;
+}
+
+template <int NR>
+__device__ __forceinline__ unsigned long long ws_load_msgs(const FusedStepParams& f, long long d, int lane,
+                                                           unsigned* buf) {
+    constexpr int S = kWsSlots / NR;
+    const int N = f.nranks;
+    unsigned long long tag = 0ull;
+    if (lane < N) tag = ld_relaxed_sys(ws_tag_ptr(f, lane, d));
+#pragma unroll
+    for (int h = 0; h < kWsSlots / 4 / 32; ++h) {  // 16-byte chunks
+        const int c = lane + 32 * h, m = (4 * c) / S;
+        if (m < N) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                         :: "r"(smem_u32(buf + 4 * c)), "l"(ws_entry_ptr(f, m, d, 4 * c - m * S)) : "memory");
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return tag;
+}
+
+// The encode front has passed ticket q: its own-rank tile carries this step's
+// tag (q >= TR, or a skipped rank: trivially).  A decode warp starts ticket c
+// only once the front has passed c + W, one decode round (about one wave of
+// the grid) later, so the tile's records have landed everywhere and one round
+// trip fetches valid tags and entries.
+__device__ __forceinline__ bool ws_front_passed(const FusedStepParams* par, int R, unsigned TR, unsigned q, int lane) {
+    int ok = 1;
+    if (lane == 0 && q < TR && !par[q % R].skip) {
+        const EncodeParams& p = par[q % R].enc;
+        ok = (unsigned)(ld_relaxed_sys(p.tags + q / R) >> 32) == p.epoch;
+    }
+    return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
+// Decode + apply tile d of rank f (rows a6-a8).  Returns false if a peer timed
+// out (nothing of this tile applied).  tag / buf: this tile's messages
+// (ws_load_msgs, its cp.async group the only one outstanding).  cw: the
+// warp's biased counts, all 0x80808080 on entry and on return.  nxt: the
+// warp's next (rank, tile) ticket; if the encode front has passed its round
+// (a probe loaded at the start), its messages go into nbuf / ntag right after
+// this tile's first target loads, so both round trips overlap.
+template <int MODE, int NR>
+__device__ __forceinline__ bool ws_decode_tile(const FusedStepParams& f, long long d, int lane,
+                                               unsigned long long tag, unsigned* buf, unsigned* cw, unsigned* bm,
+                                               unsigned nxt, const FusedStepParams* par, int R, unsigned TR,
+                                               unsigned W, unsigned* nbuf, unsigned long long& ntag,
+                                               bool& nloaded, unsigned long long* dts) {
+    const EncodeParams& p = f.enc;
+    constexpr int S = kWsSlots / NR;
+    const int N = f.nranks;
+    const unsigned stamp = entry_stamp(p.epoch);
+    // 0. probe: has the encode front passed the next ticket's own round?
+    const bool nxt_live = nxt < TR && !par[nxt % R].skip;
+    const unsigned q = nxt + W;
+    const bool q_trivial = q >= TR || par[q % R].skip;
+    unsigned long long probe = 0ull;
+    if (lane == 0 && nxt_live && !q_trivial) probe = ld_relaxed_sys(par[q % R].enc.tags + q / R);
+    // 1. every rank's tag of this step (poll with a back-off; a peer timeout
+    //    raised anywhere makes the wait give up at once)
+    bool ok = true;
+    unsigned long long t0 = 0ull;
+    for (;;) {
+        const bool ready = lane >= N || (unsigned)(tag >> 32) == p.epoch;
+        if (__all_sync(0xffffffffu, ready)) break;
+        int give_up = 0;
+        if (lane == 0) {
+            const unsigned long long now = now_ns();
+            if (t0 == 0ull) t0 = now;
+            give_up = (now - t0 > f.timeout_ns || (ld_relaxed_sys(f.flags) & kFlagPeer)) ? 1 : 0;
+        }
+        if (__shfl_sync(0xffffffffu, give_up, 0)) {
+            ok = false;
+            break;
+        }
+        __nanosleep(256);
+        if (!ready) tag = ld_relaxed_sys(ws_tag_ptr(f, lane, d));
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    if (dts) dts[4] = now_ns();
+    // 2. count the entries: lane m < N holds rank m's count, read by shuffle;
+    //    an entry of this step still stale in the copy (a record's tag can
+    //    land before its entries) is re-polled.  The first entry to touch a
+    //    float4 (claim bitmap bm) makes its lane the one that applies it.
+    const int kl = lane < N ? (int)(unsigned)tag : 0;
+    int kk[NR];  // every rank's count, in every lane
+#pragma unroll
+    for (int m = 0; m < NR; ++m) kk[m] = __shfl_sync(0xffffffffu, kl, m);
+    unsigned claimed = 0u;  // bit u: this lane applies the float4 of slot u's entry
+    bool dense = false;     // entries beyond the window: apply by a full scan
+    if (ok) {
+        // slot u of this lane is entry j = 32 u - m S + lane of rank m = 32 u / S
+        // (compile-time); all slots' loads first, then the atomics
+        unsigned ev[kWsSpec], valid = 0u;
+#pragma unroll
+        for (int u = 0; u < kWsSpec; ++u) ev[u] = buf[lane + 32 * u];
+#pragma unroll
+        for (int u = 0; u < kWsSpec; ++u) {
+            const int m = (32 * u) / S, j = 32 * u - m * S + lane;
+            if (j < kk[m]) valid |= 1u << u;
+        }
+#pragma unroll
+        for (int u = 0; u < kWsSpec; ++u) {
+            if (((valid >> u) & 1u) && (ev[u] >> kStampShift) != stamp) {
+                // rare: re-poll until this step's entry has landed
+                const int fl = lane + 32 * u, m = (32 * u) / S, j = fl - m * S;
+                const unsigned long long ts = now_ns();
+                const unsigned* a = ws_entry_ptr(f, m, d, j);
+                unsigned e;
+                do {
+                    __nanosleep(128);
+                    e = ld_relaxed_sys(a);
+                    if (now_ns() - ts > f.timeout_ns) {
+                        ok = false;
+                        break;
+                    }
+                } while ((e >> kStampShift) != stamp);
+                ev[u] = e;
+                buf[fl] = e;
+                if ((e >> kStampShift) != stamp) valid &= ~(1u << u);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kWsSpec; ++u) {
+            if ((valid >> u) & 1u) count_biased(cw, ev[u]);
+        }
+        unsigned old[kWsSpec];
+#pragma unroll
+        for (int u = 0; u < kWsSpec; ++u) {
+            const unsigned wd = (ev[u] >> 3) & (kTile / 4 - 1);
+            old[u] = ((valid >> u) & 1u) ? atomicOr(bm + (wd >> 5), 1u << (wd & 31u)) : ~0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kWsSpec; ++u)
+            if (!((old[u] >> ((ev[u] >> 3) & 31u)) & 1u)) claimed |= 1u << u;
+        // entries beyond the window (tiles denser than S / 4096): rank m's are
+        // overflow indices [ovx_m, ovx_m + ov_m)
+        const int ovl = lane < N ? max(0, kl - S) : 0;
+        int ovx = ovl;  // inclusive prefix over the lanes (ranks)
+#pragma unroll
+        for (int o = 1; o < kFusedMaxRanks; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ovx, o);
+            if (lane >= o) ovx += y;
+        }
+        const int OV = __shfl_sync(0xffffffffu, ovx, kFusedMaxRanks - 1);
+        ovx -= ovl;  // exclusive
+        dense = OV > 0;
+        const unsigned long long t_ov = OV ? now_ns() : 0ull;
+        for (int c0 = 0; c0 < OV && __all_sync(0xffffffffu, ok); c0 += 32 * kWsBatch) {
+            unsigned ov[kWsBatch];
+            const unsigned* a[kWsBatch];
+            unsigned have = 0u, pnd = 0u;
+#pragma unroll
+            for (int u = 0; u < kWsBatch; ++u) {
+                const int fo = c0 + lane + 32 * u;
+                a[u] = nullptr;
+                int m = 0;
+#pragma unroll
+                for (int qq = 1; qq < kFusedMaxRanks; ++qq)
+                    if (qq < N && __shfl_sync(0xffffffffu, ovx, qq) <= fo) m = qq;
+                const int rem = fo - __shfl_sync(0xffffffffu, ovx, m);
+                if (fo < OV) {
+                    a[u] = ws_entry_ptr(f, m, d, S + rem);
+                    ov[u] = ld_relaxed_sys(a[u]);
+                    have |= 1u << u;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kWsBatch; ++u)
+                if (((have >> u) & 1u) && (ov[u] >> kStampShift) != stamp) pnd |= 1u << u;
+            while (pnd) {
+                if (now_ns() - t_ov > f.timeout_ns) {
+                    pnd = 0u;
+                    have = 0u;
+                    ok = false;
+                    break;
+                }
+                __nanosleep(128);
+#pragma unroll
+                for (int u = 0; u < kWsBatch; ++u) {
+                    if (!((pnd >> u) & 1u)) continue;
+                    ov[u] = ld_relaxed_sys(a[u]);
+                    if ((ov[u] >> kStampShift) == stamp) pnd &= ~(1u << u);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kWsBatch; ++u)
+                if ((have >> u) & 1u) count_biased(cw, ov[u]);
+        }
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    __syncwarp();
+    if (dts) dts[5] = now_ns();
+    // 3. apply (R8): word v = lane + 32 i holds the counts of elements 4v..4v+3;
+    //    every word is reset to 0x80808080 for the warp's next tile
+    auto load_next = [&]() {
+        nloaded = false;
+        if (!nxt_live) return;
+        const int passed = q_trivial || (unsigned)(probe >> 32) == par[q % R].enc.epoch;
+        if (__shfl_sync(0xffffffffu, passed, 0)) {
+            ntag = ws_load_msgs<NR>(par[nxt % R], nxt / R, lane, nbuf);
+            nloaded = true;
+        }
+    };
+    const long long db = d * kTile;
+    auto apply_word = [&](int v, const float4& tv) {
+        const unsigned c = cw[v];
+        cw[v] = 0x80808080u;
+        const long long e0 = db + 4ll * v;
+        const int cc[4] = {(int)(c & 0xffu) - 128, (int)((c >> 8) & 0xffu) - 128, (int)((c >> 16) & 0xffu) - 128,
+                           (int)(c >> 24) - 128};
+        if (e0 + 4 <= p.n) {
+            float4 t = tv;
+            if (cc[0]) t.x = apply_count<MODE>(t.x, cc[0], p.tau, f.alpha);
+            if (cc[1]) t.y = apply_count<MODE>(t.y, cc[1], p.tau, f.alpha);
+            if (cc[2]) t.z = apply_count<MODE>(t.z, cc[2], p.tau, f.alpha);
+            if (cc[3]) t.w = apply_count<MODE>(t.w, cc[3], p.tau, f.alpha);
+            *reinterpret_cast<float4*>(f.target + e0) = t;
+        } else {
+            for (int e = 0; e < 4 && e0 + e < p.n; ++e)
+                if (cc[e]) f.target[e0 + e] = apply_count<MODE>(f.target[e0 + e], cc[e], p.tau, f.alpha);
+        }
+    };
+    bool first = true;
+    if (__any_sync(0xffffffffu, dense || !ok)) {
+        // dense tile (or an abort): every word is scanned
+        unsigned touched = 0u;
+#pragma unroll 8
+        for (int i = 0; i < kTile / 4 / 32; ++i)
+            if (cw[lane + 32 * i] != 0x80808080u) touched |= 1u << i;
+        if (!ok) {
+            for (unsigned m = touched; m; m &= m - 1u) cw[lane + 32 * (__ffs(m) - 1)] = 0x80808080u;
+            touched = 0u;
+        }
+        while (__any_sync(0xffffffffu, touched != 0u)) {
+            int iv[kWsBatch];
+            float4 tv[kWsBatch];
+#pragma unroll
+            for (int u = 0; u < kWsBatch; ++u) {
+                iv[u] = -1;
+                if (touched) {
+                    iv[u] = lane + 32 * (__ffs(touched) - 1);
+                    touched &= touched - 1u;
+                    const long long e0 = db + 4ll * iv[u];
+                    if (e0 + 4 <= p.n) tv[u] = *reinterpret_cast<const float4*>(f.target + e0);
+                }
+            }
+            if (first) {
+                load_next();
+                first = false;
+            }
+#pragma unroll
+            for (int u = 0; u < kWsBatch; ++u)
+                if (iv[u] >= 0) apply_word(iv[u], tv[u]);
+        }
+    } else {
+        // the float4s this lane claimed, from its own entries
+        while (__any_sync(0xffffffffu, claimed != 0u)) {
+            int iv[kWsBatch];
+            float4 tv[kWsBatch];
+#pragma unroll
+            for (int u = 0; u < kWsBatch; ++u) {
+                iv[u] = -1;
+                if (claimed) {
+                    const int su = __ffs(claimed) - 1;
+                    claimed &= claimed - 1u;
+                    iv[u] = (int)((buf[lane + 32 * su] >> 3) & (kTile / 4 - 1));
+                    const long long e0 = db + 4ll * iv[u];
+                    if (e0 + 4 <= p.n) tv[u] = *reinterpret_cast<const float4*>(f.target + e0);
+                }
+            }
+            if (first) {
+                load_next();
+                first = false;
+                if (dts) dts[6] = now_ns();
+            }
+#pragma unroll
+            for (int u = 0; u < kWsBatch; ++u)
+                if (iv[u] >= 0) apply_word(iv[u], tv[u]);
+        }
+    }
+    if (first) load_next();
+    __syncwarp();
+    bm[lane] = 0u;  // the claim bitmap, cleared for the warp's next tile
+    __syncwarp();
+    if (dts) dts[7] = now_ns();
+    return ok;
+}
+
+// An encode group passing over a ticket of a skipped rank (loopback test hook).
+__device__ __forceinline__ unsigned ws_pass_ticket(WsGroupSmem& G, int g, int gt, unsigned nxt) {
+    if (gt == 0) G.ticket = nxt;
+    group_bar(g);
+    const unsigned next = G.ticket;
+    group_bar(g);
+    return next;
+}
+
+// The CTA body; par[0..R) are the ranks whose work this grid does (one rank,
+// or a loopback group), in shared memory.
+template <int CMP, bool HAS_G, int MODE, int NR, bool GROUP>
+__device__ __forceinline__ void ws_cta(const FusedStepParams* par, int R_) {
+    const int R = GROUP ? R_ : 1;
+    __shared__ WsGroupSmem s_grp[kWsGroups];
+    // decode warps' arrays in dynamic shared memory (kWsDecSmem bytes per warp):
+    // biased counts (4 KB), two message buffers (2 x 1 KB), claim bitmap
+    extern __shared__ __align__(16) unsigned s_dyn[];
+    __shared__ unsigned s_tiles;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const FusedStepParams& f0 = par[0];
+    const unsigned TR = (unsigned)f0.enc.num_tiles * (unsigned)R;
+    const long long slot = blockIdx.x;
+    const bool trace = f0.trace && slot < kStepTraceCtas;
+    if (trace && tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_step_trace[slot * kStepTracePhases + 0] = now_ns();
+        g_step_trace[slot * kStepTracePhases + 5] = smid | (1u << 18);
+        s_tiles = 0u;
+    }
+    __syncthreads();
+    if (warp < kWsGroups * kTileWarps) {
+        // ---- encode group g
+        const int g = warp / kTileWarps, gt = tid - g * kTileThreads;
+        WsGroupSmem& G = s_grp[g];
+        const unsigned last = TR + gridDim.x * kWsGroups - 1u;
+        if (gt == 0) G.ticket = atomicInc(f0.ticket, last);
+        group_bar(g);
+        unsigned cur = G.ticket, done = 0u;
+        while (cur < TR) {
+            unsigned nxt = 0u;
+            if (gt == 0) nxt = atomicInc(f0.ticket, last);  // in flight during this tile
+            const FusedStepParams& f = par[cur % R];
+            if (f.skip) {
+                cur = ws_pass_ticket(G, g, gt, nxt);
+                continue;
+            }
+            cur = ws_encode_tile<CMP, HAS_G>(f, cur / R, g, gt, G, nxt);
+            ++done;
+        }
+        if (trace && gt == 0) {
+            atomicAdd(&s_tiles, done);
+            if (g == 0) g_step_trace[slot * kStepTracePhases + 1] = now_ns();
+        }
+    } else {
+        // ---- decode warp
+        const int dw = warp - kWsGroups * kTileWarps;
+        unsigned* cw = s_dyn + dw * (kWsDecSmem / 4);
+        unsigned* msg0 = cw + kTile / 4;
+        unsigned* bm = msg0 + 2 * kWsSlots;
+        bm[lane] = 0u;
+#pragma unroll
+        for (int i = 0; i < kTile / 4 / 4 / 32; ++i)
+            reinterpret_cast<uint4*>(cw)[lane + 32 * i] = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+        __syncwarp();
+        // tiles gw, gw + W, gw + 2 W, ... (static: a decode warp waits only on
+        // encodes, which never wait, so any assignment makes progress; the
+        // warps follow the encode front about one wave behind)
+        const unsigned W = gridDim.x * kWsDecWarps;
+        unsigned cur = blockIdx.x * kWsDecWarps + dw;
+        unsigned long long tag = 0ull, ntag = 0ull;
+        bool loaded = false;
+        unsigned tiles_done = 0u, b = 0u;
+        while (cur < TR) {
+            const unsigned nxt = cur + W;
+            const FusedStepParams& f = par[cur % R];
+            if (f.skip) {
+                cur = nxt;
+                loaded = false;
+                continue;
+            }
+            // debug trace (GTC_DECODE_TRACE=1): decode warp 0 of each CTA stamps
+            // (arrival, messages issued, done, loaded-ahead, tags, counted,
+            // first target loads, applied) per tile
+            const bool dtr = trace && dw == 0 && lane == 0 && tiles_done < kWsTraceTiles;
+            unsigned long long* dts = g_step_trace + kWsTraceBase + (slot * kWsTraceTiles + tiles_done) * 8;
+            if (dtr) dts[0] = now_ns(), dts[3] = loaded ? 1ull : 0ull;
+            if (!loaded) {
+                while (!ws_front_passed(par, R, TR, cur + W, lane)) __nanosleep(512);
+                tag = ws_load_msgs<NR>(f, cur / R, lane, msg0 + b * kWsSlots);
+            }
+            if (dtr) dts[1] = now_ns();
+            if (!ws_decode_tile<MODE, NR>(f, cur / R, lane, tag, msg0 + b * kWsSlots, cw, bm, nxt, par, R, TR, W,
+                                      msg0 + (b ^ 1u) * kWsSlots,
+                                      ntag, loaded, dtr ? dts : nullptr) &&
+                lane < f.nranks)
+                atomicOr_system(f.peer_flags[lane], kFlagPeer);  // GTC_EPEER on every rank
+            if (dtr) dts[2] = now_ns();
+            ++tiles_done;
+            cur = nxt;
+            if (loaded) {
+                tag = ntag;
+                b ^= 1u;
+            }
+        }
+        if (trace && dw == 0 && lane == 0) g_step_trace[slot * kStepTracePhases + 2] = now_ns();
+    }
+    if (trace) {
+        __syncthreads();
+        if (tid == 0) {
+            g_step_trace[slot * kStepTracePhases + 3] = s_tiles;
+            g_step_trace[slot * kStepTracePhases + 4] = now_ns();
+        }
+    }
+}
+
+template <int CMP, bool HAS_G, int MODE, int NR>
+__global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) gtc_step_ws_kernel(const FusedStepParams f) {
+    __shared__ FusedStepParams s_par[1];
+    {
+        const int* src = reinterpret_cast<const int*>(&f);
+        int* dst = reinterpret_cast<int*>(s_par);
+        for (int i = threadIdx.x; i < (int)(sizeof(FusedStepParams) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+    }
+    // the previous step's kernel is complete (its memory visible) before any
+    // ticket is taken: every ticket of that launch is taken by then
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    __syncthreads();
+    ws_cta<CMP, HAS_G, MODE, NR, false>(s_par, 1);
+}
+
+// Loopback group: every CTA does the work of every rank (tickets interleave
+// the ranks), so no CTA waits on a rank whose CTAs are not resident.
+template <int CMP, bool HAS_G, int MODE, int NR>
+__global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm)
+gtc_step_ws_group_kernel(const FusedStepParams* __restrict__ group, int world) {
+    __shared__ FusedStepParams s_par[kFusedMaxRanks];
+    const int* src = reinterpret_cast<const int*>(group);
+    int* dst = reinterpret_cast<int*>(s_par);
+    for (int i = threadIdx.x; i < (int)(sizeof(FusedStepParams) / sizeof(int)) * world; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    ws_cta<CMP, HAS_G, MODE, NR, true>(s_par, world);
+}
+
+// The decode warps' dynamic shared memory may exceed the 48 KB default.
+template <typename K>
+void ws_smem_attr(K kernel) {
+    static std::mutex mu;
+    static std::vector<const void*> done;  // kernels whose attribute is set
+    std::lock_guard<std::mutex> lock(mu);
+    const void* k = reinterpret_cast<const void*>(kernel);
+    if (std::find(done.begin(), done.end(), k) == done.end()) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsDecWarps * kWsDecSmem);
+        done.push_back(k);
+    }
+}
+
+// Persistent grid: every CTA slot of the device.
+int ws_grid() {
+    static std::once_flag once;
+    static int grid = 296;
+    std::call_once(once, [] {
+        int dev = 0, sms = 0, per_sm = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            (ws_smem_attr(gtc_step_ws_kernel<GTC_CMP_GT, true, GTC_ACCUM_WEIGHTS, 2>), true) &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gtc_step_ws_kernel<GTC_CMP_GT, true, GTC_ACCUM_WEIGHTS, 2>,
+                                                          kWsThreads, kWsDecWarps * kWsDecSmem) == cudaSuccess &&
+            sms > 0 && per_sm > 0)
+            grid = sms * per_sm;
+    });
+    return grid;
+}
+
 // GTC_STEP_KERNEL=grouped: the previous design (groups of encode CTAs and a
 // decode CTA, roles by blockIdx), kept for comparison
 bool grouped_kernel() {
@@ -877,6 +1499,20 @@ bool grouped_kernel() {
     }
     return v == 1;
 }
+
+// GTC_STEP_KERNEL=ticket: the ticketed one-CTA-per-tile kernel for every mode
+// (default: the warp-specialized kernel for WEIGHTS / UPDATE, the ticketed
+// one for MOMENTUM, whose dense apply is a second full stream)
+bool ticket_kernel_forced() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GTC_STEP_KERNEL");
+        v = (e && std::strcmp(e, "ticket") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+bool use_ws(int mode) { return mode != GTC_ACCUM_MOMENTUM && !grouped_kernel() && !ticket_kernel_forced(); }
 
 template <int CMP, bool HAS_G, int MODE>
 cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
@@ -893,6 +1529,19 @@ cudaError_t launch_t(FusedStepParams& f, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (grouped) return cudaLaunchKernelEx(&cfg, gtc_step_p2p_kernel<CMP, HAS_G, MODE>, f);
+    if (use_ws(MODE)) {
+        cfg.gridDim = dim3((unsigned)ws_grid());
+        cfg.blockDim = dim3(kWsThreads);
+        cfg.dynamicSmemBytes = kWsDecWarps * kWsDecSmem;
+        switch (ws_nr(f.nranks)) {
+            case 2: ws_smem_attr(gtc_step_ws_kernel<CMP, HAS_G, MODE, 2>);
+                    return cudaLaunchKernelEx(&cfg, gtc_step_ws_kernel<CMP, HAS_G, MODE, 2>, f);
+            case 4: ws_smem_attr(gtc_step_ws_kernel<CMP, HAS_G, MODE, 4>);
+                    return cudaLaunchKernelEx(&cfg, gtc_step_ws_kernel<CMP, HAS_G, MODE, 4>, f);
+            default: ws_smem_attr(gtc_step_ws_kernel<CMP, HAS_G, MODE, 8>);
+                     return cudaLaunchKernelEx(&cfg, gtc_step_ws_kernel<CMP, HAS_G, MODE, 8>, f);
+        }
+    }
     return cudaLaunchKernelEx(&cfg, gtc_step_ticket_kernel<CMP, HAS_G, MODE>, f);
 }
 
@@ -909,6 +1558,18 @@ cudaError_t launch_group_t(const FusedStepParams* group, const FusedStepParams& 
     if (grouped_kernel()) {
         const long long per_rank = Q * (kDecGroup + 1) + std::min<long long>(h.lag_groups, Q);
         gtc_step_p2p_group_kernel<CMP, HAS_G, MODE><<<(unsigned)(per_rank * world), kTileThreads, 0, s>>>(group, world);
+    } else if (use_ws(MODE)) {
+        const unsigned g = (unsigned)ws_grid(), b = kWsThreads, sm = kWsDecWarps * kWsDecSmem;
+        switch (ws_nr(world)) {
+            case 2: ws_smem_attr(gtc_step_ws_group_kernel<CMP, HAS_G, MODE, 2>);
+                    gtc_step_ws_group_kernel<CMP, HAS_G, MODE, 2><<<g, b, sm, s>>>(group, world);
+                    break;
+            case 4: ws_smem_attr(gtc_step_ws_group_kernel<CMP, HAS_G, MODE, 4>);
+                    gtc_step_ws_group_kernel<CMP, HAS_G, MODE, 4><<<g, b, sm, s>>>(group, world);
+                    break;
+            default: ws_smem_attr(gtc_step_ws_group_kernel<CMP, HAS_G, MODE, 8>);
+                     gtc_step_ws_group_kernel<CMP, HAS_G, MODE, 8><<<g, b, sm, s>>>(group, world);
+        }
     } else {
         const long long per_rank = h.enc.num_tiles + h.lag_tiles;
         gtc_step_ticket_group_kernel<CMP, HAS_G, MODE><<<(unsigned)(per_rank * world), kTileThreads, 0, s>>>(group,
