@@ -101,7 +101,7 @@ enum { GTC_EXCHANGE_P2P = 0,     /* default: peers' messages are read straight f
 
 /* gtc_step at world > 1 with the p2p exchange (OR-ed into gtc_init's flags). */
 enum { GTC_STEP_FUSED = 0,       /* default: the whole step is ONE kernel
-                                    (gtc_step_p2p_kernel)     */
+                                    (gtc_step_ticket_kernel)  */
        GTC_STEP_SPLIT = 32       /* encode + decode_apply as two kernels: faster
                                     above ~5 % update density */ };
 
@@ -309,8 +309,9 @@ gtc_status gtc_connect_loopback(gtc_ctx* const* ctxs, int world);
 /* Loopback group, every rank on ONE device: the fused one-kernel step
  * (PAPER.md:222 encode -> exchange -> aggregate -> apply; the kernel of
  * gtc_step at world > 1) of all `world` ranks as ONE launch on `stream`:
- * CTA j of rank r is block j * world + r, so every CTA a decode CTA waits on
- * has a lower block index, exactly as in the per-rank kernel.
+ * CTAs take tickets from one group counter, ticket g being CTA g / world of
+ * rank g % world, so a CTA only waits on tiles of lower tickets, exactly as
+ * in the per-rank kernel.
  *  grads[r] / residuals[r] / targets[r]: rank r's arguments of gtc_step
  *  (grads == NULL, or grads[r] == NULL on every rank: residuals hold r + g).
  *  debug_flags: bit r set = rank r's CTAs exit at once (a rank that never

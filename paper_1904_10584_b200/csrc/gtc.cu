@@ -723,9 +723,6 @@ static bool fused_step_enabled() {
 // step of this parity was not fused.
 static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha,
                              cudaStream_t stream, int ranks_per_device, FusedStepParams& f) {
-    // GTC_STEP_PULL=1 (experiment): no pushed records, decoders read the
-    // peers' tags and entries in place over NVLink
-    const bool pull = std::getenv("GTC_STEP_PULL") && std::getenv("GTC_STEP_PULL")[0] == '1';
     begin_step(c);
     const int par = seg_parity(c);
     f = FusedStepParams{};
@@ -752,7 +749,7 @@ static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, flo
         f.peer_flags[i] = &reinterpret_cast<Ctrl*>(b + c->L.ctrl)->flags;
         f.push_out[i] = nullptr;
         f.push_in[i] = nullptr;
-        if (i == c->rank || pull) continue;
+        if (i == c->rank) continue;
         // this rank's records in rank i's push region, and rank i's in ours
         unsigned char* out = b + c->L.push + ((size_t)par * c->world + c->rank) * c->L.push_slot;
         if (!c->push_clean[par]) {
@@ -764,19 +761,16 @@ static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, flo
         f.push_out[i] = out;
         f.push_in[i] = c->ws + c->L.push + ((size_t)par * c->world + i) * c->L.push_slot;
     }
-    c->push_clean[par] = !pull;
+    c->push_clean[par] = true;
     f.rank = c->rank;
     f.nranks = c->world;
-    f.lag_groups = step_p2p_lag_groups(c->num_tiles, ranks_per_device);
-    step_p2p_lags(c->num_tiles, ranks_per_device, &f.lag_tiles, &f.lag_pf);
+    f.lag_tiles = step_p2p_lag_tiles(c->num_tiles, ranks_per_device);
     f.ticket = &c->ctrl->ticket;
-    f.num_groups = (c->num_tiles + kDecGroup - 1) / kDecGroup;
     f.target = target;
     f.alpha = alpha;
     f.flags = &c->ctrl->flags;
     f.timeout_ns = c->timeout_ns;
     f.trace = decode_trace_enabled() ? 1 : 0;
-    f.diag = std::getenv("GTC_STEP_DIAG") ? std::atoi(std::getenv("GTC_STEP_DIAG")) : 0;
     return GTC_OK;
 }
 

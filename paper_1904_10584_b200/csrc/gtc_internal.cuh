@@ -37,7 +37,7 @@ struct alignas(256) Ctrl {
     unsigned long long counted;   // p2p sharded decode: the step whose owner count lists
                                   // the rank has published (sharded.cu)
     unsigned ticket;              // fused step: next CTA ticket of the running launch (wraps to
-                                  // 0 after the launch's last CTA takes its ticket; step_p2p.cu)
+                                  // 0 when the launch's last CTA takes its ticket; step_p2p.cu)
 };
 
 // Header of a contiguous message region.
@@ -132,16 +132,12 @@ struct DecodeParams {
     int trace;                     // GTC_DECODE_TRACE=1: stamp phase times (debug)
 };
 
-// The fused p2p step (step_p2p.cu): one grid of encode CTAs (one tile each,
-// rows a1-a5) interleaved with decode CTAs (kDecGroup tiles each, rows
-// a6-a8), a decode CTA following the encodes of its tiles by lag_groups
-// groups.  Each encode CTA pushes its tile's record -- tag and the first
-// kPushCap entries -- into every peer's push region with one bulk (TMA) copy
-// per peer, so the decoders read every rank's tiles from local memory;
-// entries beyond kPushCap (tiles denser than 1/8) are pulled from the
-// owner's segmented buffer over NVLink.
+// The fused p2p step (step_p2p.cu): the CTA with ticket b encodes tile b and
+// pushes its record -- tag and the first kPushCap entries -- into every peer's
+// push region with one bulk (TMA) copy per peer, and decodes tile b -
+// lag_tiles of every rank from the records pushed here (entries beyond
+// kPushCap, tiles denser than 1/8, are read from the owner over NVLink).
 constexpr int kFusedMaxRanks = 8;
-constexpr int kDecGroup = 8;
 constexpr int kPushCap = kTile / 8;
 constexpr int kPushRec = 16 + 4 * kPushCap;          // bytes per tile record: {u64 tag, u64 0, u32 entries[kPushCap]}
 struct FusedStepParams {
@@ -152,13 +148,9 @@ struct FusedStepParams {
     const unsigned char* push_in[kFusedMaxRanks];      // rank m's records in this rank's push region (null: self)
     int rank;
     int nranks;
-    int lag_groups;                                    // grouped kernel: decode group = encode group - lag_groups
-    int num_groups;                                    // grouped kernel: ceil(num_tiles / kDecGroup) (launcher)
-    int lag_tiles;                                     // ticketed kernel: CTA b encodes tile b, decodes b - lag_tiles
-    int lag_pf;                                        // ticketed kernel: ... and prefetches the targets of b - lag_pf
-    unsigned* ticket;                                  // ticketed kernel: the launch's CTA ticket counter
-                                                       // (loopback group: rank 0's, shared by the group);
-                                                       // warp-specialized kernel: its encode ticket counter
+    int lag_tiles;                                     // CTA b encodes tile b, decodes tile b - lag_tiles
+    unsigned* ticket;                                  // the launch's CTA ticket counter (Ctrl::ticket;
+                                                       // loopback group: rank 0's, shared by the group)
     float* target;
     float alpha;
     unsigned long long* flags;                         // this rank's Ctrl::flags
@@ -166,8 +158,6 @@ struct FusedStepParams {
     unsigned long long timeout_ns;                     // longest wait for a peer's tile
     int skip;                                          // loopback test hook: this rank does nothing
     int trace;                                         // GTC_DECODE_TRACE=1: phase stamps (debug)
-    int diag;                                          // GTC_STEP_DIAG (experiments only): 1 blockIdx roles,
-                                                       // 2 no target RMW, 4 no decode (results invalid)
 };
 
 // Owner-computes (sharded) decode, GTC_DECODE_SHARDED (sharded.cu; SURVEY
@@ -241,8 +231,7 @@ cudaError_t launch_step_p2p(FusedStepParams& p, int cmp_mode, int accum_mode, cu
 // caller); `host` holds the same parameters for the launch configuration.
 cudaError_t launch_step_p2p_group(const FusedStepParams* group, const FusedStepParams& host, int world,
                                   int cmp_mode, int accum_mode, cudaStream_t s);
-int step_p2p_lag_groups(int num_tiles, int ranks_per_device);
-void step_p2p_lags(int num_tiles, int ranks_per_device, int* lag_tiles, int* lag_pf);
+int step_p2p_lag_tiles(int num_tiles, int ranks_per_device);
 cudaError_t read_step_trace(unsigned long long* host, int max_entries);
 cudaError_t read_decode_trace(unsigned long long* host, int max_entries);
 bool decode_trace_enabled();

@@ -13,8 +13,8 @@ mappings).  The kernels are the production ones:
     yet queued); with GTC_DECODE_SHARDED the owner count (gtc_exchange) and
     the list apply (gtc_decode_apply);
   - fused path: gtc_step_group, the one-kernel encode -> push -> decode ->
-    apply step of EVERY rank as ONE launch (rank r's CTA j is block j*world+r,
-    so no launch waits on another launch).
+    apply step of EVERY rank as ONE launch (ticket g is CTA g/world of rank
+    g%world, so no launch waits on another launch).
 
 Every rank's message, k, integer counts, residual, weights (or momentum
 buffer) and the replica hash are compared with an N-worker oracle step
@@ -188,7 +188,7 @@ def test_loopback_sharded_tiny_and_more_ranks_than_tiles():
 ])
 def test_loopback_fused_parity(world, lag, accum, cmp, monkeypatch):
     """gtc_step_group: the fused kernel of every rank in one launch, with the
-    default decode lag and with short lags (decode CTAs then wait on tiles
+    default decode lag and with short lags (CTAs then wait on tiles
     still being encoded: stamped entries, re-polls)."""
     if lag is not None:
         monkeypatch.setenv("GTC_FUSED_LAG", lag)

@@ -14,42 +14,11 @@ import synth  # noqa: E402
 
 def report(rank, tr):
     t = tr.reshape(-1, 6).astype(np.int64)
-    if (t[0, 5] >> 18) & 1:  # warp-specialized kernel: CTA slots below 2048, decode-warp stamps after
-        t = t[:2048]
     ncta = int(np.max(np.nonzero(t[:, 0])[0])) + 1
     t = t[:ncta]
-    if ((t[:, 5] >> 18) & 1).all():          # warp-specialized persistent kernel: one slot per CTA
-        ph = t[:, :5].astype(np.float64)
-        base = ph[:, 0].min()
-        st, enc_end, dec_end, en = [(ph[:, i] - base) / 1e3 for i in (0, 1, 2, 4)]
-        tiles = t[:, 3]
-        print(f"[rank {rank}] warp-specialized grid {ncta} CTAs: kernel span {en.max():.1f} us; CTA start "
-              f"max {st.max():.1f} us", flush=True)
-        if "TRACE_US_PER_STEP" in os.environ:
-            print(f"  step - span (launch gap): {float(os.environ['TRACE_US_PER_STEP']) - en.max():.1f} us", flush=True)
-        print(f"  encode group 0 done p50/max {np.median(enc_end):.1f}/{enc_end.max():.1f} us; decode warp 0 done "
-              f"p50/max {np.median(dec_end):.1f}/{dec_end.max():.1f} us; tiles per CTA min/p50/max "
-              f"{tiles.min()}/{int(np.median(tiles))}/{tiles.max()}", flush=True)
-        dt = tr[2048 * 6: 2048 * 6 + ncta * 24 * 8].reshape(ncta, 24, 8).astype(np.int64)
-        have = dt[:, :, 2] > 0
-        if have.any():
-            arr = (dt[:, :, 0] - int(base)) / 1e3
-            ph = lambda a, b: (dt[:, :, b] - dt[:, :, a]) / 1e3  # noqa: E731
-            parts = [("front wait + loads", 0, 1), ("tags", 1, 4), ("count", 4, 5), ("scan + 1st loads", 5, 6),
-                     ("apply", 6, 7), ("ret", 7, 2)]
-            ahead = dt[:, :, 3]
-            print("  decode warp 0 per tile p50/p90 (us): " + ", ".join(
-                f"{nm} {np.median(ph(a, b)[have]):.2f}/{np.percentile(ph(a, b)[have], 90):.2f}" for nm, a, b in parts) +
-                f"; messages loaded ahead {100 * ahead[have].mean():.0f} %", flush=True)
-            for i in range(min(int(have.sum(axis=1).max()), 24)):
-                col = have[:, i]
-                if col.any():
-                    print(f"    tile #{i}: arrival p50 {np.median(arr[col, i]):.1f} us: " + ", ".join(
-                        f"{nm} {np.median(ph(a, b)[col, i]):.2f}" for nm, a, b in parts), flush=True)
-        return
-    dec = (t[:, 5] >> 16) & 1 == 1          # decodes a tile (grouped: a decode CTA)
-    donly = (t[:, 5] >> 17) & 1 == 1        # ticketed kernel: decode-only tail CTA
-    ticketed = bool(donly.any()) or os.environ.get("GTC_STEP_KERNEL", "") != "grouped"
+    dec = (t[:, 5] >> 16) & 1 == 1          # decodes a tile
+    donly = (t[:, 5] >> 17) & 1 == 1        # decode-only tail CTA
+    ticketed = True
     ph = t[:, :5].astype(np.float64)
     base = ph[:, 0].min()
     st, en = (ph[:, 0] - base) / 1e3, (ph[:, 4] - base) / 1e3
