@@ -96,6 +96,14 @@ gtc_status bmuf_sync_sim(bmuf_ctx* ctx, float* const* w_locals, int nmodels, flo
 /* Eq. (5): zeta = C * N * (1 - eta). */
 double bmuf_zeta(double C, int N, double eta);
 
+/* Collective (every rank calls it; world > 1): wait for the device, then an
+ * NCCL barrier, so no peer still reads or pushes into this rank's workspace.
+ * Call it before bmuf_destroy and before freeing the workspace. */
+gtc_status bmuf_quiesce(bmuf_ctx* ctx);
+
+/* Destroy the communicator and the peer mappings; never frees caller memory.
+ * Local: no collective (run bmuf_quiesce on every rank first when peers may
+ * still access this workspace). */
 void bmuf_destroy(bmuf_ctx* ctx);
 
 #ifdef __cplusplus

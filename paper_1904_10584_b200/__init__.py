@@ -90,6 +90,7 @@ _SIGS = {
     "bmuf_check": (_i32, [_vp]),
     "bmuf_sync_sim": (_i32, [_vp, _vp, _i32, _vp, _vp, _f32, _f32, _vp]),
     "bmuf_zeta": (ctypes.c_double, [ctypes.c_double, _i32, ctypes.c_double]),
+    "bmuf_quiesce": (_i32, [_vp]),
     "bmuf_destroy": (None, [_vp]),
 }
 
@@ -615,6 +616,10 @@ def bmuf_zeta(C: float, N: int, eta: float) -> float:
     return load_library().bmuf_zeta(C, N, eta)
 
 
+def bmuf_quiesce(ctx):
+    _chk(load_library().bmuf_quiesce(ctx), "bmuf_quiesce")
+
+
 def bmuf_destroy(ctx):
     load_library().bmuf_destroy(ctx)
 
@@ -684,12 +689,20 @@ class BMUF:
                   self.eta, self.zeta, _stream(stream, self.device))
 
     def close(self):
+        """Collective at world > 1 (every rank calls it): quiesce, then destroy."""
         if getattr(self, "ctx", None) is not None:
-            bmuf_destroy(self.ctx)
-            self.ctx = None
+            try:
+                if self.world > 1:
+                    bmuf_quiesce(self.ctx)
+            finally:
+                bmuf_destroy(self.ctx)
+                self.ctx = None
 
     def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
+        # never a collective here: ranks collect garbage at different times
+        if getattr(self, "ctx", None) is not None:
+            try:
+                bmuf_destroy(self.ctx)
+            except Exception:
+                pass
+            self.ctx = None

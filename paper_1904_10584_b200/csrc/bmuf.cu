@@ -450,15 +450,24 @@ gtc_status bmuf_sync_sim(bmuf_ctx* c, float* const* w_locals, int nmodels, float
 
 double bmuf_zeta(double C, int N, double eta) { return C * (double)N * (1.0 - eta); }
 
+gtc_status bmuf_quiesce(bmuf_ctx* c) {
+    if (!c) return GTC_EINVAL;
+    if (!(c->comm && c->ws && c->world > 1)) return GTC_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != c->device) cudaSetDevice(c->device);
+    gtc_status s = GTC_OK;
+    if (cudaDeviceSynchronize() != cudaSuccess) s = GTC_ECUDA;
+    int* one = reinterpret_cast<int*>(c->ws + kIpcOff);
+    if (s == GTC_OK && ncclAllReduce(one, one, 1, ncclInt32, ncclSum, c->comm, 0) != ncclSuccess) s = GTC_ENCCL;
+    if (s == GTC_OK && cudaStreamSynchronize(0) != cudaSuccess) s = GTC_ECUDA;
+    if (prev != c->device) cudaSetDevice(prev);
+    return s;
+}
+
 void bmuf_destroy(bmuf_ctx* c) {
     if (!c) return;
-    if (c->comm && c->ws && c->world > 1) {  // no peer may still be reading or pushing into this workspace
-        cudaSetDevice(c->device);
-        cudaDeviceSynchronize();
-        int* one = reinterpret_cast<int*>(c->ws + kIpcOff);
-        if (ncclAllReduce(one, one, 1, ncclInt32, ncclSum, c->comm, 0) == ncclSuccess) cudaStreamSynchronize(0);
-        gtc::ipc_unmap(c->peer_alloc);
-    }
+    if (c->ws && c->world > 1) gtc::ipc_unmap(c->peer_alloc);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
