@@ -223,6 +223,26 @@ def test_loopback_fused_dense_tiles_pull_over(world, monkeypatch):
     run.close()
 
 
+def test_loopback_fused_grid_changes_between_steps(monkeypatch):
+    """The ticket counter wraps to 0 at the end of every launch, so
+    consecutive fused steps with different grids (T + L CTAs, L changed by
+    GTC_FUSED_LAG) each hand out tickets 0 .. T + L - 1: a leftover count
+    would give CTAs out-of-range tickets and skip tiles."""
+    n, tau, world = 400_009, 8.0, 2
+    run = Run(n, tau, world, "gt", "weights")
+    for t, lag in enumerate(["3", "97", None, "1", "40", None]):
+        if lag is None:
+            monkeypatch.delenv("GTC_FUSED_LAG", raising=False)
+        else:
+            monkeypatch.setenv("GTC_FUSED_LAG", lag)
+        gs = grads_for("correlated", n, tau, t, world)
+        assert run.grp.step([to_dev(g) for g in gs], run.rd, run.wd, -0.5) == gtc.GTC_OK
+        torch.cuda.synchronize()
+        om, oc, _ = run.oracle_step(gs, -0.5)
+        run.check(om, oc, f"lag {lag} step {t}")
+    run.close()
+
+
 def test_loopback_alternating_fused_and_split(monkeypatch):
     """Fused and split steps interleaved: the push records of a parity whose
     last step was split are cleared before the next fused step of it."""
