@@ -25,16 +25,17 @@ def sources():
         glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "gtc.h")]
 
 
-def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=(), csrc: str = None) -> str:
     """Compile every csrc/*.cu into `out` (default: the in-tree libgtc.so);
-    `defines` (-D flags) only for experiment builds (tools/build_variant.py)."""
-    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
+    `defines` (-D flags) and another `csrc` directory only for experiment
+    builds (tools/build_variant.py)."""
+    srcs = sorted(glob.glob(os.path.join(csrc or os.path.join(PKG, "csrc"), "*.cu")))
     newest = max(os.path.getmtime(s) for s in sources())
-    if not force and not defines and os.path.exists(out) and os.path.getmtime(out) >= newest:
+    if not force and not defines and not csrc and os.path.exists(out) and os.path.getmtime(out) >= newest:
         return out
     nccl = _nccl_root()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"), "-I", os.path.join(nccl, "include"),
            "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
            f"-Xlinker=-rpath={os.path.join(nccl, 'lib')}",
            *[f"-D{d}" for d in defines], "-o", out + ".tmp", *srcs]
