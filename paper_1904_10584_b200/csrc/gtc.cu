@@ -152,8 +152,6 @@ struct gtc_ctx {
     FusedStepParams* host_group = nullptr;  // loopback rank 0: pinned staging of the group parameters
     int packed_rank = -1;           // whose message the contiguous region holds (-1: stale)
     bool push_clean[2] = {true, true};  // p2p: the last step of this parity was fused (or none yet)
-    cudaStream_t s2_stream = nullptr;   // GTC_STEP_2S experiment: the decode kernel's stream
-    cudaEvent_t s2_start = nullptr, s2_done = nullptr;
 
     long long* host_kx = nullptr;  // pinned, 2 * world
     std::vector<long long> last_k;
@@ -781,25 +779,6 @@ static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual,
     FusedStepParams f;
     gtc_status s = fill_fused(c, grad, residual, target, alpha, stream, 1, f);
     if (s != GTC_OK) return s;
-    static const bool two_stream = std::getenv("GTC_STEP_2S") && std::getenv("GTC_STEP_2S")[0] == '1';
-    if (two_stream && mode != GTC_ACCUM_MOMENTUM) {  // experiment (step_2s.cu): no pushes, decode pulls
-        if (!c->s2_stream) {
-            cudaError_t e = cudaStreamCreateWithFlags(&c->s2_stream, cudaStreamNonBlocking);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->s2_start, cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->s2_done, cudaEventDisableTiming);
-            if (e != cudaSuccess) return cuda_fail(c, e, "step: two-stream setup");
-        }
-        for (int i = 0; i < c->world; ++i) {
-            f.push_in[i] = nullptr;
-            f.push_out[i] = nullptr;
-        }
-        c->push_clean[seg_parity(c)] = false;
-        cudaError_t e = launch_step_2s(f, c->cmp_mode, mode, stream, c->s2_stream, c->s2_start, c->s2_done);
-        if (e != cudaSuccess) return cuda_fail(c, e, "step: two-stream launch");
-        c->launches += 2;
-        c->stage = Stage::kBound;
-        return GTC_OK;
-    }
     cudaError_t e = launch_step_p2p(f, c->cmp_mode, mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "step: fused p2p launch");
     c->launches += 1;
@@ -1174,9 +1153,6 @@ void gtc_destroy(gtc_ctx* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->host_kx) cudaFreeHost(c->host_kx);
     if (c->host_group) cudaFreeHost(c->host_group);
-    if (c->s2_stream) cudaStreamDestroy(c->s2_stream);
-    if (c->s2_start) cudaEventDestroy(c->s2_start);
-    if (c->s2_done) cudaEventDestroy(c->s2_done);
     delete c;
 }
 
