@@ -1,10 +1,14 @@
-# A/B on one box: the ticketed kernel now (per-thread decode waits) vs the committed one (tools/exp_base)
+# A/B on one box: the working-tree ticketed kernel vs the committed one (tools/exp_base; build_variant --csrc)
 set -x
-O=gpurun_out/r02ab; mkdir -p $O
+O=gpurun_out/r02ab2; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 python tools/build_variant.py /tmp/base.so --csrc tools/exp_base >> $O/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_loopback.py -q -x > $O/pytest_loopback.log 2>&1; echo "EXIT $?" >> $O/pytest_loopback.log
 TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1"
-for i in 1 2; do
-GTC_DECODE_TRACE=1 timeout 300 $TR --master-port 2960$i tools/step_trace.py > $O/trace_new$i.txt 2>&1
-GTC_LIB=/tmp/base.so GTC_DECODE_TRACE=1 timeout 300 $TR --master-port 2961$i tools/step_trace.py > $O/trace_base$i.txt 2>&1
-done
+B="bench.py --gpus 2 --no-e2e --no-cpu-baseline --steps 1000"
+p=29600
+for rho in 0.01 0.1; do for i in 1 2; do
+p=$((p+1)); timeout 300 $TR --master-port $p $B --rho $rho > $O/bench_new_${rho}_$i.jsonl 2> /dev/null
+p=$((p+1)); GTC_LIB=/tmp/base.so timeout 300 $TR --master-port $p $B --rho $rho > $O/bench_base_${rho}_$i.jsonl 2> /dev/null
+done; done
+timeout 900 python -m pytest tests/test_multigpu.py -q -x -k "fused" > $O/pytest_multigpu.log 2>&1; echo "EXIT $?" >> $O/pytest_multigpu.log
