@@ -578,7 +578,7 @@ def run_gtc(args):
     kern_ms = ms_per_step if one_kernel else phases[0]
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     # DRAM traffic per launch from the committed warm, back-to-back ncu capture
-    traffic, traffic_src = None, None
+    traffic, traffic_src, loopback_traffic = None, None, None
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tpath):
         try:
@@ -589,6 +589,18 @@ def run_gtc(args):
                 traffic, traffic_src = tj[key]["dram_bytes_per_launch"], tj[key]["source"]
         except Exception:
             traffic = None
+    if traffic is None and world > 1 and one_kernel:
+        # ncu never wraps a multi-rank run: the committed capture of this
+        # kernel is its loopback-group form (both ranks on one GPU), per rank
+        try:
+            with open(tpath) as f:
+                lb = json.load(f).get(f"loopback_{args.workload}/n{world}/{args.accum}/fused")
+            if lb and lb.get("rho_target") == args.rho:
+                traffic_src = ("not this run: " + lb["source"] + ", per rank of a world-%d loopback group on one "
+                               "GPU (dram_traffic_loopback_per_rank)" % world)
+                loopback_traffic = lb["dram_bytes_per_launch"]
+        except Exception:
+            pass
     roofline = {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "alg_bytes_per_launch": alg_bytes, "ms_per_launch": kern_ms, "peak_source": peak_src,
@@ -596,6 +608,8 @@ def run_gtc(args):
                 "frac_sector_floor": floor_bytes / (kern_ms * 1e-3) / 1e9 / peak,
                 "touched_elements": nnz_c, "touched_sectors": sectors_c,
                 "share_of_step": kern_ms / ms_per_step}
+    if loopback_traffic is not None:
+        roofline["dram_traffic_loopback_per_rank"] = loopback_traffic
     if world > 1:
         roofline["nvlink"] = {
             "bytes_per_step_per_rank": nvl_bytes if one_kernel else 4 * (world - 1) * max(k_all_mean),

@@ -34,6 +34,8 @@
 #include "bmuf.h"
 #include "gtc_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -377,8 +379,8 @@ gtc_status bmuf_check(bmuf_ctx* c) {
     return err ? GTC_EPEER : GTC_OK;
 }
 
-gtc_status bmuf_sync(bmuf_ctx* c, float* w_local, float* wg_shard, float* delta_shard, float eta, float zeta,
-                     cudaStream_t stream) {
+static gtc_status bmuf_sync_impl(bmuf_ctx* c, float* w_local, float* wg_shard, float* delta_shard, float eta,
+                                 float zeta, cudaStream_t stream) {
     if (!c) return GTC_EINVAL;
     if (c->shard > 0 && (!w_local || !wg_shard || !delta_shard)) return GTC_EINVAL;
     if (!aligned16(w_local) || !aligned16(wg_shard) || !aligned16(delta_shard)) return GTC_EALIGN;
@@ -424,6 +426,14 @@ gtc_status bmuf_sync(bmuf_ctx* c, float* w_local, float* wg_shard, float* delta_
         ncclAllGather(mine, w_local, (size_t)c->shard, ncclFloat32, c->comm, stream) != ncclSuccess)
         st = GTC_ENCCL;
     if (prev != c->device) cudaSetDevice(prev);
+    return st;
+}
+
+gtc_status bmuf_sync(bmuf_ctx* c, float* w_local, float* wg_shard, float* delta_shard, float eta, float zeta,
+                     cudaStream_t stream) {
+    nvtxRangePushA("bmuf_sync");  // phase tracing (gtc.cu)
+    const gtc_status st = bmuf_sync_impl(c, w_local, wg_shard, delta_shard, eta, zeta, stream);
+    nvtxRangePop();
     return st;
 }
 

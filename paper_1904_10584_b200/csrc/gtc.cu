@@ -29,6 +29,8 @@
 
 #include "gtc_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 using namespace gtc;
 
 namespace {
@@ -164,6 +166,14 @@ struct gtc_ctx {
 };
 
 namespace {
+
+// Phase tracing: every API call is an NVTX range (header-only NVTX v3, a no-op
+// unless a profiler is attached), so a timeline shows encode / exchange /
+// decode_apply / step per rank next to the kernels they enqueue.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 gtc_status fail(gtc_ctx* c, gtc_status s, const std::string& what) {
     if (c) c->detail = what;
@@ -487,6 +497,7 @@ static gtc_status encode_impl(gtc_ctx* c, const float* grad, float* residual, cu
 }
 
 gtc_status gtc_encode(gtc_ctx* c, const float* grad, float* residual, cudaStream_t stream) {
+    NvtxRange nvtx("gtc_encode");
     return encode_impl(c, grad, residual, stream, nullptr, 0.f, GTC_ACCUM_WEIGHTS);
 }
 
@@ -596,6 +607,7 @@ static gtc_status exchange_nccl(gtc_ctx* c, cudaStream_t stream) {
 }
 
 gtc_status gtc_exchange(gtc_ctx* c, cudaStream_t stream) {
+    NvtxRange nvtx("gtc_exchange");
     if (!c) return GTC_EINVAL;
     if (c->stage != Stage::kEncoded) return fail(c, GTC_ESTATE, "exchange: no encode since the last exchange");
     if (c->sharded) {
@@ -697,6 +709,7 @@ static gtc_status decode_launch(gtc_ctx* c, float* target, float alpha, int mode
 
 gtc_status gtc_decode_apply(gtc_ctx* c, float* target, float alpha, int mode, int8_t* counts_out,
                             cudaStream_t stream) {
+    NvtxRange nvtx("gtc_decode_apply");
     if (!c) return GTC_EINVAL;
     if (c->stage != Stage::kExchanged) return fail(c, GTC_ESTATE, "decode_apply: call gtc_exchange first");
     gtc_status s = check_apply_args(c, target, mode);
@@ -788,6 +801,7 @@ static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual,
 
 gtc_status gtc_step(gtc_ctx* c, const float* grad, float* residual, float* target, float alpha, int mode,
                     cudaStream_t stream) {
+    NvtxRange nvtx("gtc_step");
     if (c && c->world == 1) {
         // world 1: the aggregate is this rank's own quanta (c = +-1 on its
         // message), so the encode kernel applies them itself: one launch per step
@@ -859,6 +873,7 @@ gtc_status gtc_connect_loopback(gtc_ctx* const* ctxs, int world) {
 
 gtc_status gtc_step_group(gtc_ctx* const* ctxs, int world, const float* const* grads, float* const* residuals,
                           float* const* targets, float alpha, int mode, uint32_t debug_flags, cudaStream_t stream) {
+    NvtxRange nvtx("gtc_step_group");
     if (!ctxs || world < 2 || world > kFusedMaxRanks || !residuals || !targets) return GTC_EINVAL;
     gtc_ctx* c0 = ctxs[0];
     if (!c0 || !c0->host_group) return fail(c0, GTC_EINVAL, "step_group: ctxs[0] is not rank 0 of a loopback group");
