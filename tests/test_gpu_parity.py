@@ -450,3 +450,26 @@ def test_config5_fused_step_1e9_sampled():
         assert np.array_equal(bits(rd[a:b]), rw.view(np.uint32)), a
         assert np.array_equal(bits(wd[a:b]), ww.view(np.uint32)), a
     ctx.close()
+
+
+def test_serialized_message_matches_oracle_in_spec_layout():
+    """A GPU message in SPEC.md:202's wire format (gtc_wire_pack over
+    gtc_read_message): header and SPEC-layout words equal the oracle's
+    message converted by hand (bit 31 = sign, bits 0..30 = index),
+    and unpacking returns the canonical words."""
+    import struct
+
+    n, tau = 2 * gtc.GTC_TILE + 777, 8.0
+    g = synth.correlated_gradient(n, 4.0, synth.BASE_SEED, 0, 0)
+    r0 = synth.uniform(n, -tau, tau, synth.rank_seed(0))
+    ctx = gtc.GTC(n, tau)
+    ctx.encode(to_dev(g), to_dev(r0.copy()))
+    blob = ctx.serialize_message()
+    words, _ = oracle.encode(g, r0.copy(), tau, oracle.CMP_GT)
+    assert blob[:4] == b"GTCU"
+    assert struct.unpack_from("<QfI", blob, 4) == (n, tau, words.size)
+    spec = np.frombuffer(blob, dtype="<u4", offset=20)
+    assert np.array_equal(spec, ((words & 1) << 31) | (words >> 1))
+    back, dim, t = gtc.gtc_wire_unpack(blob)
+    assert np.array_equal(back, words) and dim == n and t == tau
+    ctx.close()
