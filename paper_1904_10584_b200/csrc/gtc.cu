@@ -792,14 +792,6 @@ static gtc_status step_fused_p2p(gtc_ctx* c, const float* grad, float* residual,
     FusedStepParams f;
     gtc_status s = fill_fused(c, grad, residual, target, alpha, stream, 1, f);
     if (s != GTC_OK) return s;
-    static const bool pair = std::getenv("GTC_STEP_PAIR") && std::getenv("GTC_STEP_PAIR")[0] == '1';
-    if (pair) {  // experiment (step_pair.cu)
-        cudaError_t e = launch_step_pair(f, c->cmp_mode, mode, stream);
-        if (e != cudaSuccess) return cuda_fail(c, e, "step: pair launch");
-        c->launches += 2;
-        c->stage = Stage::kBound;
-        return GTC_OK;
-    }
     cudaError_t e = launch_step_p2p(f, c->cmp_mode, mode, stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "step: fused p2p launch");
     c->launches += 1;

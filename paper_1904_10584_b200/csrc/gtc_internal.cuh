@@ -232,7 +232,6 @@ cudaError_t launch_step_p2p(FusedStepParams& p, int cmp_mode, int accum_mode, cu
 cudaError_t launch_step_p2p_group(const FusedStepParams* group, const FusedStepParams& host, int world,
                                   int cmp_mode, int accum_mode, cudaStream_t s);
 int step_p2p_lag_tiles(int num_tiles, int ranks_per_device);
-cudaError_t launch_step_pair(const FusedStepParams& f, int cmp_mode, int accum_mode, cudaStream_t s);
 cudaError_t read_step_trace(unsigned long long* host, int max_entries);
 cudaError_t read_decode_trace(unsigned long long* host, int max_entries);
 bool decode_trace_enabled();
