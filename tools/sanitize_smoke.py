@@ -1,7 +1,8 @@
 """Small exerciser of every kernel path for compute-sanitizer (memcheck /
 racecheck / synccheck / initcheck): ragged sizes, both comparison modes,
-fused step, counting decode with dump, simulated messages, packing,
-and the persistent encode variant when GTC_ENCODE_VARIANT=persistent."""
+fused world-1 step, counting decode with dump, simulated messages, packing,
+and a world-2 loopback group (the ticketed fused step, the split p2p calls
+and the owner-computes decode) on one GPU."""
 import os
 import sys
 
@@ -35,6 +36,18 @@ def main():
             ctx.decode_apply_msgs([md, md[: max(0, md.numel() // 2)], md], w, 1.0, gtc.GTC_ACCUM_WEIGHTS, cnt)
             assert ctx.check() in (gtc.GTC_OK, gtc.GTC_ENONFINITE)
             ctx.close()
+    for n in (4097, 3 * 4096 + 1234):
+        for sharded in (False, True):
+            tau = 1.0
+            grp = gtc.LoopbackGroup(n, tau, 2, dev, sharded=sharded)
+            gs = [torch.from_numpy(synth.normal(n, 1, n, r) * np.float32(0.8)).to(dev) for r in range(2)]
+            rs = [torch.from_numpy(synth.uniform(n, -tau, tau, 2, n, r)).to(dev) for r in range(2)]
+            ws = [torch.zeros(n, device=dev) for _ in range(2)]
+            if not sharded:
+                grp.step(gs, rs, ws, -0.5)                    # ticketed fused kernel, one launch
+            grp.split_step(gs, rs, ws, -0.5)                  # separate p2p calls (or owner count + apply)
+            assert grp.check() == [gtc.GTC_OK] * 2
+            grp.close()
     torch.cuda.synchronize()
     print("sanitize smoke done")
 
