@@ -102,8 +102,9 @@ enum { GTC_EXCHANGE_P2P = 0,     /* default: peers' messages are read straight f
 /* gtc_step at world > 1 with the p2p exchange (OR-ed into gtc_init's flags). */
 enum { GTC_STEP_FUSED = 0,       /* default: the whole step is ONE kernel
                                     (gtc_step_ticket_kernel)  */
-       GTC_STEP_SPLIT = 32       /* encode + decode_apply as two kernels: faster
-                                    above ~5 % update density */ };
+       GTC_STEP_SPLIT = 32       /* encode + decode_apply as two kernels (kept for
+                                    comparison: slower at every measured density
+                                    and world size)          */ };
 
 /* gtc_init flag: one rank of a LOOPBACK group -- all `world` ranks are
  * contexts of ONE process (tests and single-process drivers; no NCCL
