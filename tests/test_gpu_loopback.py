@@ -223,6 +223,32 @@ def test_loopback_fused_dense_tiles_pull_over(world, monkeypatch):
     run.close()
 
 
+@pytest.mark.parametrize("world", [5, 8])
+@pytest.mark.parametrize("path", ["fused", "split", "sharded"])
+def test_loopback_up_to_8_ranks(world, path, monkeypatch):
+    """World 5 and 8 (kFusedMaxRanks): the N = 8 configs of BASELINE.json
+    cannot run on the harness's at most 4 GPUs, so their code paths -- 8
+    ranks' records per decode, speculative windows of 32 entries per rank and
+    the overflow rounds beyond them, 7 pushes per tile, 8 owners -- are
+    checked here, bit-exact against the N-worker oracle."""
+    n, tau = 150_011, 8.0
+    run = Run(n, tau, world, "gt", "weights", sharded=(path == "sharded"))
+    kinds = ["correlated", "dense", "dyadic"]
+    for t in range(3):
+        if path == "fused":
+            monkeypatch.setenv("GTC_FUSED_LAG", ["5", "1", "40"][t])
+        gs = grads_for(kinds[t], n, tau, t, world)
+        gd = [to_dev(g) for g in gs]
+        if path == "fused":
+            assert run.grp.step(gd, run.rd, run.wd, -0.5) == gtc.GTC_OK
+        else:
+            run.grp.split_step(gd, run.rd, run.wd, -0.5)
+        torch.cuda.synchronize()
+        om, oc, _ = run.oracle_step(gs, -0.5)
+        run.check(om, oc, f"{path} world={world} step {t} ({kinds[t]})")
+    run.close()
+
+
 def test_loopback_fused_grid_changes_between_steps(monkeypatch):
     """The ticket counter wraps to 0 at the end of every launch, so
     consecutive fused steps with different grids (T + L CTAs, L changed by
