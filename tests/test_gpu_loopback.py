@@ -319,6 +319,23 @@ def test_loopback_lstm_am_size_fused_world4():
     run.close()
 
 
+@pytest.mark.parametrize("rho", [0.0001, 0.01, 0.1])
+def test_loopback_config4_density_sweep_fused_world8(rho):
+    """C4 (BASELINE.json configs[3]: density 0.01 %-10 %, 8 workers) through the
+    fused one-kernel step itself: a world-8 loopback group at the LSTM-AM
+    size, one step per density, bit-exact against the 8-worker oracle."""
+    n, tau, world = synth.LSTM_AM_PARAMS, 8.0, 8
+    sigma = synth.sigma_for_density(rho, tau, synth.mean_abs_scale(n))
+    run = Run(n, tau, world, "gt", "weights")
+    gs = [synth.lstm_gradient(n, sigma, synth.BASE_SEED, 0, w, 0.5) for w in range(world)]
+    assert run.grp.step([to_dev(g) for g in gs], run.rd, run.wd, -1e-3) == gtc.GTC_OK
+    torch.cuda.synchronize()
+    om, oc, _ = run.oracle_step(gs, -1e-3)
+    assert abs(sum(m.size for m in om) / (world * n) - rho) < 0.5 * rho  # the intended density regime
+    run.check(om, oc, f"lstm_am world=8 rho={rho}")
+    run.close()
+
+
 # ------------------------------------------------------------------ failure semantics
 def test_loopback_fused_missing_peer_raises_epeer_everywhere(monkeypatch):
     """A rank that never shows up (debug bit): the others time out, and EVERY
