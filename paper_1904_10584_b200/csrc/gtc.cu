@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "gtc_internal.cuh"
+#include "tile_encode.cuh"  // kTileThreads, entry_stamp (host side of the fused step parameters)
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -777,6 +778,11 @@ static gtc_status fill_fused(gtc_ctx* c, const float* grad, float* residual, flo
     c->push_clean[par] = true;
     f.rank = c->rank;
     f.nranks = c->world;
+    f.spec_window = kTileThreads / c->world;
+    f.spec_shift = -1;
+    for (int sh = 0; sh < 9; ++sh)
+        if ((1 << sh) == f.spec_window) f.spec_shift = sh;
+    f.stamp = entry_stamp(c->epoch);
     f.lag_tiles = step_p2p_lag_tiles(c->num_tiles, ranks_per_device);
     f.ticket = &c->ctrl->ticket;
     f.target = target;

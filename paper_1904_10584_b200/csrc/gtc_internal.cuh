@@ -149,6 +149,9 @@ struct FusedStepParams {
     int rank;
     int nranks;
     int lag_tiles;                                     // CTA b encodes tile b, decodes tile b - lag_tiles
+    int spec_window;                                   // speculative entries per rank, kTileThreads / nranks
+    int spec_shift;                                    // log2(spec_window) if a power of two, else -1
+    unsigned stamp;                                    // entry_stamp(enc.epoch)
     unsigned* ticket;                                  // the launch's CTA ticket counter (Ctrl::ticket;
                                                        // loopback group: rank 0's, shared by the group)
     float* target;

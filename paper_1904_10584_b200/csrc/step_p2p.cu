@@ -157,8 +157,10 @@ __device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b
         if (tid == kTileThreads - 1) prev_ld = ld_tag_count(p.tags + te);
         load_tile<HAS_G>(p, base, full_tile, tid, rv, gv);
     }
-    const int S = kTileThreads / N;  // speculative entries per rank: thread tid reads entry sj of rank sm
-    const int sm = tid / S, sj = tid - sm * S;
+    // speculative entries per rank (S = 256 / N, host-computed): thread tid
+    // reads entry sj of rank sm (a shift when S is a power of two)
+    const int S = f.spec_window;
+    const int sm = f.spec_shift >= 0 ? tid >> f.spec_shift : tid / S, sj = tid - sm * S;
     unsigned long long tagv = 0ull;
     unsigned spec = 0u;
     if (dec) {
@@ -177,7 +179,7 @@ __device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b
         tile_scan_ballots(sel, lane, warp, my_off, s_scan);
     }
     if (dec && tid < N) s_k[tid] = ((unsigned)(tagv >> 32) == p.epoch) ? (int)(unsigned)tagv : -1;
-    const unsigned stamp = entry_stamp(p.epoch);
+    const unsigned stamp = f.stamp;  // entry_stamp(p.epoch), host-computed
     __syncthreads();
     if (te >= 0 && warp == kTileWarps - 1) {
         const unsigned incl = tile_scan_finish(lane, s_scan);
@@ -225,8 +227,7 @@ __device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b
             if (sm < N && sj < s_k[sm]) count_biased(s_cw, spec);
             // entries [S, k_m) of every rank (dense tiles); beyond kPushCap
             // they come from the owner's buffer over NVLink
-            int OV = 0;
-            for (int m = 0; m < N; ++m) OV += max(0, s_k[m] - S);
+            const int OV = __reduce_add_sync(0xffffffffu, lane < N ? max(0, s_k[lane] - S) : 0);
             const unsigned long long t_ov = OV ? now_ns() : 0ull;
             for (int c0 = 0; c0 < OV && !failed; c0 += kOvPerThread * kTileThreads) {
                 unsigned ov[kOvPerThread];
@@ -304,21 +305,17 @@ __device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b
         const unsigned total = s_misc[0], prev = s_misc[1];
         unsigned* dst = p.seg + base;
         unsigned* s_ent = reinterpret_cast<unsigned*>(s_rec + 2);
-        if (total != 0) {
-#pragma unroll
-            for (int j = 0; j < kTileVec; ++j) {
-                unsigned o = s_scan[j * kTileWarps + warp] + my_off[j];
-                const unsigned l0 = (unsigned)(j * kTileThreads + tid) * 4u;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if ((sel >> (4 * j + e)) & 1u) {
-                        const unsigned w = make_entry(stamp, l0 + e, (neg >> (4 * j + e)) & 1u);
-                        st_relaxed_sys(dst + o, w);
-                        if (o < (unsigned)kPushCap) s_ent[o] = w;
-                        ++o;
-                    }
-                }
-            }
+        // only the thread's selected elements (a few per thread at 1 %): its
+        // word's slot is its (round, warp) base + the words before it in the
+        // thread's round (my_off packed one byte per round: <= 124 each)
+        const unsigned offs = my_off[0] | (my_off[1] << 8) | (my_off[2] << 16) | (my_off[3] << 24);
+        for (unsigned m = sel; m; m &= m - 1u) {
+            const int bi = __ffs(m) - 1, j = bi >> 2;
+            const unsigned o = s_scan[j * kTileWarps + warp] + ((offs >> (8 * j)) & 0xffu) +
+                               __popc(sel & ((1u << bi) - 1u) & (0xfu << (4 * j)));
+            const unsigned w = make_entry(stamp, (unsigned)(j * kTileThreads + tid) * 4u + (bi & 3), (neg >> bi) & 1u);
+            st_relaxed_sys(dst + o, w);
+            if (o < (unsigned)kPushCap) s_ent[o] = w;
         }
         for (unsigned o = total + tid; o < prev; o += kTileThreads) st_relaxed_sys(dst + o, 0u);
         const unsigned clr = min(max(total, prev), (unsigned)kPushCap);
@@ -348,7 +345,7 @@ __device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b
     stamp_ph(3);
     // ---- apply stores: u = fl(c * tau); WEIGHTS fmaf(alpha, u, t), UPDATE
     // fl(t + u) (R8) on the touched elements; MOMENTUM (M1) on every element
-    if (apply) {
+    if (apply && todo) {
 #pragma unroll
         for (int h = 0; h < kTileVec; ++h) {
             if (!((todo >> h) & 1u)) continue;

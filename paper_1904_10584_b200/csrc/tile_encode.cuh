@@ -123,7 +123,7 @@ __device__ __forceinline__ void quantize(float4 (&rv)[kTileVec], const float4 (&
             nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
             const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
             const bool ng = v < 0.0f;
-            const float rn = sl ? (ng ? __fadd_rn(v, tau) : __fsub_rn(v, tau)) : v;
+            const float rn = sl ? __fsub_rn(v, copysignf(tau, v)) : v;  // v - (-tau) == v + tau exactly
             set_comp(rv[j], e, rn);
             sel |= (unsigned)sl << (j * 4 + e);
             neg |= (unsigned)(sl && ng) << (j * 4 + e);
@@ -198,22 +198,17 @@ template <bool STAMPED, bool RELAXED = false>
 __device__ __forceinline__ void store_words(unsigned* dst, long long base, int tid, unsigned sel, unsigned neg,
                                             const unsigned (&my_off)[kTileVec], const unsigned* s_scan, int warp,
                                             unsigned total, unsigned prev_total, unsigned stamp) {
-    if (total != 0) {
-#pragma unroll
-        for (int j = 0; j < kTileVec; ++j) {
-            unsigned o = s_scan[j * kTileWarps + warp] + my_off[j];
-            const unsigned l0 = (unsigned)(j * kTileThreads + tid) * 4u;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if ((sel >> (4 * j + e)) & 1u) {
-                    const unsigned ng = (neg >> (4 * j + e)) & 1u;
-                    const unsigned w = STAMPED ? make_entry(stamp, l0 + e, ng) : (((unsigned)base + l0 + e) << 1) | ng;
-                    if (RELAXED) st_relaxed_sys(dst + o, w);
-                    else dst[o] = w;
-                    ++o;
-                }
-            }
-        }
+    // only the thread's selected elements: its word's slot is its (round,
+    // warp) base + the words before it in the thread's round
+    const unsigned offs = my_off[0] | (my_off[1] << 8) | (my_off[2] << 16) | (my_off[3] << 24);
+    for (unsigned m = sel; m; m &= m - 1u) {
+        const int bi = __ffs(m) - 1, j = bi >> 2;
+        const unsigned o = s_scan[j * kTileWarps + warp] + ((offs >> (8 * j)) & 0xffu) +
+                           __popc(sel & ((1u << bi) - 1u) & (0xfu << (4 * j)));
+        const unsigned l = (unsigned)(j * kTileThreads + tid) * 4u + (bi & 3), ng = (neg >> bi) & 1u;
+        const unsigned w = STAMPED ? make_entry(stamp, l, ng) : (((unsigned)base + l) << 1) | ng;
+        if (RELAXED) st_relaxed_sys(dst + o, w);
+        else dst[o] = w;
     }
     if (STAMPED) {
         for (unsigned o = total + tid; o < prev_total; o += kTileThreads) {
