@@ -48,6 +48,11 @@ namespace {
 // kStepTraceCtas tickets stamps %globaltimer at: start, every rank's tag of
 // the decode tile seen, counts done, apply stores issued, end; and
 // (SM id | decodes << 16 | decode-only << 17).
+#ifdef GTC_STEP_TRACE
+constexpr bool kTraceBuild = true;
+#else
+constexpr bool kTraceBuild = false;  // production builds carry no trace code (tools/step_trace.py)
+#endif
 constexpr int kStepTraceCtas = 16384;
 constexpr int kStepTracePhases = 6;
 __device__ unsigned long long g_step_trace[kStepTraceCtas * kStepTracePhases];
@@ -128,7 +133,7 @@ __device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b
     const long long te = b < T ? b : -1;       // tile encoded here
     const long long td = b - f.lag_tiles;      // tile decoded here
     const bool dec = td >= 0 && td < T;
-    const bool trace = f.trace && tid == 0 && trace_slot < kStepTraceCtas;
+    const bool trace = kTraceBuild && f.trace && tid == 0 && trace_slot < kStepTraceCtas;
     auto stamp_ph = [&](int ph) {
         if (trace) g_step_trace[trace_slot * kStepTracePhases + ph] = now_ns();
     };
@@ -344,8 +349,32 @@ __device__ __forceinline__ void ticket_cta(const FusedStepParams& f, long long b
 
     stamp_ph(3);
     // ---- apply stores: u = fl(c * tau); WEIGHTS fmaf(alpha, u, t), UPDATE
-    // fl(t + u) (R8) on the touched elements; MOMENTUM (M1) on every element
-    if (apply && todo) {
+    // fl(t + u) (R8) on the touched elements; MOMENTUM (M1) on every element.
+    // Sparse warps (no lane with more than 2 touched float4s: most warps at 1 %)
+    // visit only the touched float4s; denser ones the unrolled 4.
+    auto store_one = [&](long long e0, float4 t, unsigned c) {
+        const int cc[4] = {(int)(c & 0xffu) - 128, (int)((c >> 8) & 0xffu) - 128, (int)((c >> 16) & 0xffu) - 128,
+                           (int)(c >> 24) - 128};
+        if (e0 + 4 <= p.n) {
+            if (cc[0]) t.x = apply_count<MODE>(t.x, cc[0], p.tau, f.alpha);
+            if (cc[1]) t.y = apply_count<MODE>(t.y, cc[1], p.tau, f.alpha);
+            if (cc[2]) t.z = apply_count<MODE>(t.z, cc[2], p.tau, f.alpha);
+            if (cc[3]) t.w = apply_count<MODE>(t.w, cc[3], p.tau, f.alpha);
+            *reinterpret_cast<float4*>(f.target + e0) = t;
+        } else {
+            for (int e = 0; e < 4 && e0 + e < p.n; ++e)
+                if (cc[e]) f.target[e0 + e] = apply_count<MODE>(f.target[e0 + e], cc[e], p.tau, f.alpha);
+        }
+    };
+    const bool sparse_warp = MODE != GTC_ACCUM_MOMENTUM && !__any_sync(0xffffffffu, __popc(todo) > 2);
+    if (apply && sparse_warp) {
+        for (unsigned m = todo; m; m &= m - 1u) {
+            const int h = __ffs(m) - 1;
+            const float4 t = h == 0 ? tv[0] : h == 1 ? tv[1] : h == 2 ? tv[2] : tv[3];
+            const unsigned c = h == 0 ? cw[0] : h == 1 ? cw[1] : h == 2 ? cw[2] : cw[3];
+            store_one(db + 4ll * (tid + h * kTileThreads), t, c);
+        }
+    } else if (apply && todo) {
 #pragma unroll
         for (int h = 0; h < kTileVec; ++h) {
             if (!((todo >> h) & 1u)) continue;

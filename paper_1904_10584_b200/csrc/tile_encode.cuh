@@ -122,13 +122,13 @@ __device__ __forceinline__ void quantize(float4 (&rv)[kTileVec], const float4 (&
             const float a = fabsf(v);
             nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
             const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
-            const bool ng = v < 0.0f;
             const float rn = sl ? __fsub_rn(v, copysignf(tau, v)) : v;  // v - (-tau) == v + tau exactly
             set_comp(rv[j], e, rn);
             sel |= (unsigned)sl << (j * 4 + e);
-            neg |= (unsigned)(sl && ng) << (j * 4 + e);
+            neg |= (__float_as_uint(v) >> 31) << (j * 4 + e);  // the sign bit (v < 0 for a selected v)
         }
     }
+    neg &= sel;
 }
 
 __device__ __forceinline__ void store_residual(const EncodeParams& p, long long base, bool full_tile, int tid,

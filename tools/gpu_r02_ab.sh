@@ -1,6 +1,6 @@
 # A/B on one box: the working tree vs the committed sources (tools/exp_base; build_variant --csrc), N=1 and N=2
 set -x
-O=gpurun_out/r02ab4; mkdir -p $O
+O=gpurun_out/r02ab5; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 python tools/build_variant.py /tmp/base.so --csrc tools/exp_base >> $O/build.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_loopback.py tests/test_gpu_parity.py -q -x > $O/pytest.log 2>&1; echo "EXIT $?" >> $O/pytest.log

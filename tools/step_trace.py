@@ -1,5 +1,10 @@
 """torchrun diagnostic of the fused p2p step (GTC_DECODE_TRACE=1): per-CTA
-phase times of one traced step at the LSTM-AM size, on every rank."""
+phase times of one traced step at the LSTM-AM size, on every rank.
+
+The production library carries no trace code; build a traced one and select it:
+    python tools/build_variant.py /tmp/trace.so GTC_STEP_TRACE
+    GTC_LIB=/tmp/trace.so GTC_DECODE_TRACE=1 torchrun ... tools/step_trace.py
+"""
 import os
 import sys
 
