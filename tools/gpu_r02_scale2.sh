@@ -1,0 +1,19 @@
+# round 2, after the instruction diet: N = 1, 2, 4 lines on one 4-GPU box (fused step, 1 % and 10 %, momentum,
+# 1e9 params), the N=2 / N=4 torchrun parity suite, and a traced N=2 / N=4 step
+set -x
+O=gpurun_out/r02scale2; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+python tools/build_variant.py /tmp/trace.so GTC_STEP_TRACE >> $O/build.log 2>&1
+timeout 600 python bench.py > $O/bench_n1.jsonl 2> $O/e_n1
+timeout 600 python bench.py --no-cpu-baseline --no-e2e --rho 0.1 > $O/bench_n1_rho10.jsonl 2> $O/e_n1r
+timeout 900 python bench.py --workload 1e9 --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_n1_1e9.jsonl 2> $O/e_n1g
+p=29700
+for N in 2 4; do
+  TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1"
+  p=$((p+1)); timeout 600 $TR --master-port $p bench.py --gpus $N > $O/bench_n${N}.jsonl 2> $O/e_n$N
+  p=$((p+1)); timeout 600 $TR --master-port $p bench.py --gpus $N --no-e2e --rho 0.1 > $O/bench_n${N}_rho10.jsonl 2> $O/e_n${N}r
+  p=$((p+1)); timeout 600 $TR --master-port $p bench.py --gpus $N --no-e2e --accum momentum > $O/bench_n${N}_mom.jsonl 2> $O/e_n${N}m
+  p=$((p+1)); timeout 900 $TR --master-port $p bench.py --gpus $N --workload 1e9 --steps 20 --warmup 3 --no-e2e > $O/bench_n${N}_1e9.jsonl 2> $O/e_n${N}g
+  p=$((p+1)); GTC_LIB=/tmp/trace.so GTC_DECODE_TRACE=1 timeout 300 $TR --master-port $p tools/step_trace.py > $O/trace_n${N}.txt 2>&1
+done
+timeout 1500 python -m pytest tests/test_multigpu.py -q > $O/pytest_multigpu_4gpu.log 2>&1; echo "EXIT $?" >> $O/pytest_multigpu_4gpu.log
