@@ -106,8 +106,28 @@ __device__ __forceinline__ void load_tile(const EncodeParams& p, long long base,
     }
 }
 
+// Packed fp32 pairs (sm_100: FADD2): two IEEE round-to-nearest adds /
+// subtracts in one instruction, each lane exactly the scalar __fadd_rn /
+// __fsub_rn (R12).
+__device__ __forceinline__ float2 fadd2_rn(float2 a, float2 b) {
+    float2 c;
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0, %1}, rc;\n\t}"
+        : "=f"(c.x), "=f"(c.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return c;
+}
+__device__ __forceinline__ float2 fsub2_rn(float2 a, float2 b) {
+    float2 c;
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0, %1}, rc;\n\t}"
+        : "=f"(c.x), "=f"(c.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return c;
+}
+
 // Rows a1-a3 on the thread's 16 elements: v = fl(r + g); sel = |v| > tau (GT)
 // or >= tau (GE); r = sel ? fl(v -+ tau) : v.  rv holds the new residual.
+// Elements go in pairs through the packed adds; v - copysign(tau, v) is
+// v - tau or v + tau exactly as the scalar forms.
 template <int CMP, bool HAS_G>
 __device__ __forceinline__ void quantize(float4 (&rv)[kTileVec], const float4 (&gv)[kTileVec], float tau,
                                          unsigned& sel, unsigned& neg, bool& nonfinite) {
@@ -117,18 +137,28 @@ __device__ __forceinline__ void quantize(float4 (&rv)[kTileVec], const float4 (&
 #pragma unroll
     for (int j = 0; j < kTileVec; ++j) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float v = HAS_G ? __fadd_rn(comp(rv[j], e), comp(gv[j], e)) : comp(rv[j], e);
-            const float a = fabsf(v);
-            nonfinite |= !(a <= 3.402823466e38f);  // NaN or Inf
-            const bool sl = (CMP == GTC_CMP_GT) ? (a > tau) : (a >= tau);
-            const float rn = sl ? __fsub_rn(v, copysignf(tau, v)) : v;  // v - (-tau) == v + tau exactly
-            set_comp(rv[j], e, rn);
-            sel |= (unsigned)sl << (j * 4 + e);
-            neg |= (__float_as_uint(v) >> 31) << (j * 4 + e);  // the sign bit (v < 0 for a selected v)
+        for (int h = 0; h < 2; ++h) {
+            float2 v = h == 0 ? make_float2(rv[j].x, rv[j].y) : make_float2(rv[j].z, rv[j].w);
+            if (HAS_G) v = fadd2_rn(v, h == 0 ? make_float2(gv[j].x, gv[j].y) : make_float2(gv[j].z, gv[j].w));
+            const float2 q = fsub2_rn(v, make_float2(copysignf(tau, v.x), copysignf(tau, v.y)));
+            const float ax = fabsf(v.x), ay = fabsf(v.y);
+            nonfinite |= !(ax <= 3.402823466e38f) || !(ay <= 3.402823466e38f);  // NaN or Inf
+            const bool sx = (CMP == GTC_CMP_GT) ? (ax > tau) : (ax >= tau);
+            const bool sy = (CMP == GTC_CMP_GT) ? (ay > tau) : (ay >= tau);
+            const float2 rn = make_float2(sx ? q.x : v.x, sy ? q.y : v.y);
+            if (h == 0) {
+                rv[j].x = rn.x;
+                rv[j].y = rn.y;
+            } else {
+                rv[j].z = rn.x;
+                rv[j].w = rn.y;
+            }
+            const int b = j * 4 + 2 * h;
+            sel |= ((unsigned)sx << b) | ((unsigned)sy << (b + 1));
+            neg |= ((__float_as_uint(v.x) >> 31) << b) | ((__float_as_uint(v.y) >> 31) << (b + 1));
         }
     }
-    neg &= sel;
+    neg &= sel;  // the sign bit is v < 0 for a selected v
 }
 
 __device__ __forceinline__ void store_residual(const EncodeParams& p, long long base, bool full_tile, int tid,
