@@ -4,7 +4,7 @@
 // updates"), aggregate and apply ("The received sparse gradient updates are
 // aggregated and weights are updated based on the aggregate").
 //
-// gtc_step_ticket_kernel: T + L CTAs of 256 threads, 4 per SM.  The CTA with
+// gtc_step_ticket_kernel: T + L CTAs of 256 threads, 5 per SM.  The CTA with
 // ticket b (the order in which CTAs start, one atomicInc each) encodes tile b
 // (rows a1-a5, b < T), pushes the tile's record (tag + first kPushCap stamped
 // entries) to every peer with one bulk (TMA) copy each, and decodes tile
@@ -426,7 +426,10 @@ __device__ __forceinline__ unsigned take_ticket(unsigned* counter, unsigned last
 }
 
 template <int CMP, bool HAS_G, int MODE>
-__global__ void __launch_bounds__(kTileThreads, 4) gtc_step_ticket_kernel(const FusedStepParams f) {
+#ifndef GTC_TICKET_CTAS
+#define GTC_TICKET_CTAS 5  // resident CTAs per SM: 48 registers (measured 4 / 5 / 6: DESIGN.md §6)
+#endif
+__global__ void __launch_bounds__(kTileThreads, GTC_TICKET_CTAS) gtc_step_ticket_kernel(const FusedStepParams f) {
     const unsigned b = take_ticket(f.ticket, gridDim.x - 1u);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
