@@ -425,10 +425,10 @@ __device__ __forceinline__ unsigned take_ticket(unsigned* counter, unsigned last
     return s_ticket;
 }
 
-template <int CMP, bool HAS_G, int MODE>
 #ifndef GTC_TICKET_CTAS
 #define GTC_TICKET_CTAS 5  // resident CTAs per SM: 48 registers (measured 4 / 5 / 6: DESIGN.md §6)
 #endif
+template <int CMP, bool HAS_G, int MODE>
 __global__ void __launch_bounds__(kTileThreads, GTC_TICKET_CTAS) gtc_step_ticket_kernel(const FusedStepParams f) {
     const unsigned b = take_ticket(f.ticket, gridDim.x - 1u);
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kTileThreads, GTC_TICKET_CTAS) gtc_step_ticket
 // counter); ticket g is CTA g / world of rank g % world, so every tile a CTA
 // waits on (a lower CTA index of any rank) belongs to a lower ticket.
 template <int CMP, bool HAS_G, int MODE>
-__global__ void __launch_bounds__(kTileThreads, 4)
+__global__ void __launch_bounds__(kTileThreads, GTC_TICKET_CTAS)
 gtc_step_ticket_group_kernel(const FusedStepParams* __restrict__ group, int world) {
     __shared__ FusedStepParams s_f;
     const unsigned g = take_ticket(group[0].ticket, gridDim.x - 1u);

@@ -1,7 +1,7 @@
 # ncu source-level capture (instructions and stall samples per line) of the N=1 step kernel and of the
 # ticketed N>1 kernel (world-2 loopback group), one launch each
 set -x
-O=gpurun_out/r02src; mkdir -p $O
+O=gpurun_out/r02src2; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 B="python bench.py --no-e2e --no-cpu-baseline"
 timeout 600 $B --steps 300 --warmup 5 > $O/plain.jsonl 2>/dev/null
