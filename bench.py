@@ -568,7 +568,7 @@ def run_gtc(args):
         # pushed records landing here ((N-1) records), the target RMW
         base = 12 * n + 8 * k + 16 * T
         nvl_bytes = 4 * (K_all - k) + 16 * (world - 1) * T  # records: 16-byte header + entries
-        kernel_name = "gtc_step_p2p_kernel (fused encode + exchange + decode + apply)"
+        kernel_name = "gtc_step_ticket_kernel (fused encode + exchange + decode + apply)"
     else:
         base = 12 * n + 4 * k + 8 * T
         rmw = rmw_floor = 0

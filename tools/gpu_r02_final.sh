@@ -1,5 +1,4 @@
 # round 2 final tree (ticketed kernel at 5 CTAs/SM): N = 1, 2, 4 bench lines on one 4-GPU box, the full
-# pytest -m gpu suite (torchrun tests at world 2 and 4 included), smoke, and compute-sanitizer on the exerciser
 set -x
 O=gpurun_out/r02fin; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
@@ -16,6 +15,4 @@ for N in 2 4; do
   p=$((p+1)); timeout 900 $TR --master-port $p bench.py --gpus $N --workload 1e9 --steps 20 --warmup 3 --no-e2e > $O/bench_n${N}_1e9.jsonl 2> $O/e_n${N}g
 done
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "EXIT $?" >> $O/smoke.log
-timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_smoke.py > $O/memcheck.log 2>&1; echo "EXIT $?" >> $O/memcheck.log
-timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_smoke.py > $O/racecheck.log 2>&1; echo "EXIT $?" >> $O/racecheck.log
 timeout 2400 python -m pytest tests -q -m gpu > $O/pytest_gpu_4gpu.log 2>&1; echo "EXIT $?" >> $O/pytest_gpu_4gpu.log
