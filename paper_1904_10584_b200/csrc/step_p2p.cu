@@ -491,13 +491,14 @@ cudaError_t launch_group_g(const FusedStepParams* group, const FusedStepParams& 
 
 }  // namespace
 
-// Decode lag in tiles: one wave of resident CTAs of one rank (the tiles the
-// other ranks encode concurrently: their records have landed by then unless a
-// rank is more than a wave behind).  GTC_FUSED_LAG (tiles) overrides; tests
+// Decode lag in tiles: 1.5 waves of resident CTAs of one rank (a wave is the
+// tiles the other ranks encode concurrently; the extra half wave covers ranks
+// that run behind: measured 0.5-3 waves, DESIGN.md §6, 1.5 is fastest at
+// N = 2 and 4, rho = 1 % and 10 %).  GTC_FUSED_LAG (tiles) overrides; tests
 // use short lags so that CTAs wait on tiles still being encoded.
 int step_p2p_lag_tiles(int num_tiles, int ranks_per_device) {
     static std::once_flag once;
-    static int wave = 592;
+    static int wave = 740;  // 148 SMs x 5 CTAs, if the occupancy query fails
     std::call_once(once, [] {
         int dev = 0, sms = 0, per_sm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -507,7 +508,7 @@ int step_p2p_lag_tiles(int num_tiles, int ranks_per_device) {
             sms > 0 && per_sm > 0)
             wave = sms * per_sm;
     });
-    int w = wave / std::max(1, ranks_per_device);
+    int w = wave * 3 / 2 / std::max(1, ranks_per_device);
     if (const char* e = std::getenv("GTC_FUSED_LAG")) {  // read per step: tests vary it
         if (std::atoi(e) > 0) w = std::atoi(e);
     }

@@ -20,7 +20,7 @@ static_assert(kTileVec * kTileWarps == 32, "one (round, warp) scan entry per lan
 
 // ---------------------------------------------------------------- p2p entries
 // In p2p mode a rank's segmented message is read by its peers while it may
-// still be being written (the fused step reads tile t of every rank one wave
+// still be being written (the fused step reads tile t of every rank a lag
 // after it was encoded, with no fence on the writer's side).  Every 32-bit
 // entry of a tile slot therefore carries the step that wrote it:
 //     entry = stamp(epoch) << 13 | local << 1 | neg,   local = index - tile * kTile (< 4096)

@@ -1,6 +1,6 @@
 # round 2 final tree (ticketed kernel at 5 CTAs/SM): N = 1, 2, 4 bench lines on one 4-GPU box, the full
 set -x
-O=gpurun_out/r02fin; mkdir -p $O
+O=${O:-gpurun_out/r02fin}; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 600 python bench.py > $O/bench_n1.jsonl 2> $O/e_n1
 timeout 600 python bench.py --no-cpu-baseline --no-e2e --rho 0.1 > $O/bench_n1_rho10.jsonl 2> $O/e_n1r

@@ -2,7 +2,7 @@
 # step kernel, and the ticketed N>1 kernel through a loopback group (world 2):
 # warm DRAM traffic (20 back-to-back launches) and one full capture
 set -x
-O=gpurun_out/r02ncu2; mkdir -p $O
+O=${O:-gpurun_out/r02ncu2}; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 B="python bench.py --no-e2e --no-cpu-baseline"
 timeout 600 $B --steps 400 --warmup 5 > $O/plain_n1.jsonl 2> $O/plain_n1.err && \
